@@ -1,0 +1,152 @@
+/*
+ * vc3_b200.h — C ABI of the B200 (sm_100a) inline 3-vector codec.
+ *
+ * Drop-in boundary for the hot path of the reference package `vc3`
+ * (/root/reference/pkg/src/vc3).  The reference's Python layer binds numba
+ * kernels (_kernels.py) through codec.py / bench.py; each entry point below
+ * replaces one of those bindings (cited per function).  Differences by design:
+ *   - vectors are array-of-structs float32 [n][3] (the reference splits them
+ *     into three contiguous columns first, codec.py:70-83; we read the caller's
+ *     (n, 3) array directly and skip those passes);
+ *   - a layout travels by value (vc3_layout) and a policy as a bit mask;
+ *   - every call is asynchronous on the caller's CUDA stream (`stream` is a
+ *     cudaStream_t passed as void*; NULL = legacy default stream);
+ *   - all pointers are DEVICE pointers unless the name ends in _host;
+ *   - the library allocates nothing per call; callers own every buffer.
+ *
+ * Return value: VC3_OK (0) or a negative vc3_status.  Validation happens before
+ * any launch (the reference validates before its kernels, codec.py:70-83,
+ * bench.py:34,47, layout.py:47-69).  Non-finite input cannot be detected before
+ * the kernel on a device: compress counts offending vectors into the
+ * caller-provided device counter `d_nonfinite` (may be NULL) and the host shim
+ * raises NonFiniteInput after the stream sync (errors.py:12).
+ */
+#ifndef VC3_B200_H
+#define VC3_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* BitLayout (layout.py:38-45): widths s,e,m,p,t (sum 64) and exponent bias. */
+typedef struct vc3_layout {
+    int32_t sign_bits;
+    int32_t exponent_bits;
+    int32_t mantissa_bits;
+    int32_t phi_bits;
+    int32_t theta_bits;
+    int32_t exponent_bias;
+} vc3_layout;
+
+/* PrecisionPolicy (layout.py:119-155) as bits; a clear bit means double. */
+#define VC3_THETA_SINGLE 1u
+#define VC3_PHI_SINGLE 2u
+#define VC3_QUANT_SINGLE 4u
+#define VC3_POLICY_DEFAULT (VC3_THETA_SINGLE | VC3_QUANT_SINGLE)                   /* layout.py:183 */
+#define VC3_POLICY_ORACLE 0u                                                       /* layout.py:184 */
+#define VC3_POLICY_ALL_SINGLE (VC3_THETA_SINGLE | VC3_PHI_SINGLE | VC3_QUANT_SINGLE) /* layout.py:185 */
+
+typedef enum vc3_status {
+    VC3_OK = 0,
+    VC3_ERR_LAYOUT = -1,    /* BadLayout (layout.py:47-69)                  */
+    VC3_ERR_ARG = -2,       /* bad pointer / negative length / bad policy   */
+    VC3_ERR_CUDA = -3,      /* launch or runtime failure (vc3_last_cuda_error) */
+    VC3_ERR_NONFINITE = -4, /* NonFiniteInput (host-synchronous entry points) */
+    VC3_ERR_LENGTH = -5     /* LengthMismatch (bench.py:34,47)              */
+} vc3_status;
+
+/* Version / diagnostics */
+const char* vc3_version(void);
+const char* vc3_status_string(int status);
+int vc3_last_cuda_error(void);
+/* layout.py:47-69 validation, without raising */
+int vc3_validate_layout(vc3_layout layout);
+
+/* ---- the hot path -------------------------------------------------------- */
+
+/* codec.compress (codec.py:189-202) -> _kernels.compress_kernel (_kernels.py:215-220).
+ * xyz: float32 [n][3]; words: uint64 [n]. */
+int vc3_compress(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout,
+                 uint32_t policy, int32_t* d_nonfinite, void* stream);
+
+/* codec.decompress (codec.py:205-228) -> decompress_kernel_tab/_direct
+ * (_kernels.py:293-331).  words: uint64 [n]; xyz: float32 [n][3]. */
+int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout,
+                   void* stream);
+
+/* bench.add_compressed (bench.py:41-69) -> add_compressed_kernel (_kernels.py:348-359):
+ * c = compress(decompress(a) + decompress(b)) fused, nothing uncompressed
+ * touches memory.  The reference's default policy here is ALL_SINGLE. */
+int vc3_add_compressed(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t n,
+                       vc3_layout layout, uint32_t policy, void* stream);
+
+/* bench.add_raw (bench.py:30-38) -> add_raw_kernel (_kernels.py:341-345):
+ * the uncompressed float32 baseline, c[i] = a[i] + b[i] over n_floats floats. */
+int vc3_add_raw(const float* a, const float* b, float* c, int64_t n_floats, void* stream);
+
+/* No reference symbol: y_out = compress(alpha*decompress(x) + decompress(y)).
+ * float32 ops: t = alpha*x (rounded), then t + y (rounded), per component.
+ * y_out may alias y (in-place update). */
+int vc3_axpy(float alpha, const uint64_t* x, const uint64_t* y, uint64_t* y_out, int64_t n,
+             vc3_layout layout, uint32_t policy, void* stream);
+
+/* Low-storage (2N) RK stage on compressed registers (SURVEY §8a R18,
+ * PAPER.md:135,336), all three operands stored compressed:
+ *   dq' = a*dq + dt*R ;  q' = q + b*dq'
+ * float32 per component, each product and sum rounded in that order; q' uses
+ * the register value of dq' (before it is re-compressed).  q and dq are
+ * updated in place (40 B of HBM traffic per vector). */
+int vc3_rk_stage(float a, float b, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
+                 int64_t n, vc3_layout layout, uint32_t policy, void* stream);
+
+/* ---- pieces (codec.py:99-186) -------------------------------------------- */
+
+/* codec.to_spherical (codec.py:99-114) -> spherical_kernel (_kernels.py:223-229) */
+int vc3_to_spherical(const float* xyz, double* r, double* theta, double* phi, int64_t n,
+                     uint32_t policy, int32_t* d_nonfinite, void* stream);
+/* codec.quantize_angles (codec.py:122-140) -> quantize_kernel (_kernels.py:232-237) */
+int vc3_quantize_angles(const double* theta, const double* phi, int64_t* n_theta,
+                        int64_t* n_phi, int64_t n, vc3_layout layout, uint32_t policy,
+                        void* stream);
+/* codec.dequantize_angles (codec.py:143-153) -> dequantize_kernel (_kernels.py:334-338) */
+int vc3_dequantize_angles(const int64_t* n_theta, const int64_t* n_phi, double* theta,
+                          double* phi, int64_t n, vc3_layout layout, void* stream);
+/* codec.encode_magnitude (codec.py:156-175) -> encode_mag_kernel (_kernels.py:240-243) */
+int vc3_encode_magnitude(const double* r, uint64_t* field, int64_t n, vc3_layout layout,
+                         void* stream);
+/* codec.decode_magnitude (codec.py:178-186) -> decode_mag_kernel (_kernels.py:246-249) */
+int vc3_decode_magnitude(const int64_t* field, float* r, int64_t n, vc3_layout layout,
+                         void* stream);
+/* codec.magnitude_event_counts (codec.py:241-262): d_counts[0] += flushed,
+ * d_counts[1] += saturated (caller zeroes them). */
+int vc3_magnitude_events(const float* xyz, int64_t n, vc3_layout layout,
+                         unsigned long long* d_counts, void* stream);
+
+/* ---- statistics (analysis.py:118-167) ------------------------------------ */
+
+/* Per-chunk error moments of e_i = ||v_i - vh_i||_2 (optionally / ||v_i||), in
+ * double: for chunk k (chunk vectors each, last one ragged) writes
+ * d_chunk_stats[4k..4k+3] = (count, mean, M2, max).  Chunks merge on the host
+ * (or across ranks) in chunk order exactly like analysis._Welford. */
+int vc3_error_stats(const float* v, const float* vh, int64_t n, int32_t normalised,
+                    int64_t chunk, double* d_chunk_stats, void* stream);
+
+/* ---- host-buffer entry points (reference-facing, synchronous) ------------
+ * Same operations on HOST arrays: the call streams chunks host->device, runs
+ * the kernel and copies results back, overlapping copies and compute on
+ * internal streams.  Pinned host memory gives full PCIe/C2C bandwidth;
+ * pageable memory works but is slower.  Returns after the results are in
+ * the host buffer.  device: CUDA ordinal to run on. */
+int vc3_add_compressed_host(const uint64_t* a_host, const uint64_t* b_host, uint64_t* c_host,
+                            int64_t n, vc3_layout layout, uint32_t policy, int32_t device);
+int vc3_compress_host(const float* xyz_host, uint64_t* words_host, int64_t n, vc3_layout layout,
+                      uint32_t policy, int64_t* nonfinite_out, int32_t device);
+int vc3_decompress_host(const uint64_t* words_host, float* xyz_host, int64_t n,
+                        vc3_layout layout, int32_t device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VC3_B200_H */

@@ -1,0 +1,77 @@
+"""In-tree build of the CUDA library (``lib/libvc3_b200.so``) with nvcc.
+
+sm_100a only.  Numerics flags are part of the contract with the reference's
+IEEE arithmetic: no FMA contraction (``-fmad=false``; FMAs are written
+explicitly where proven safe), no flush-to-zero, IEEE division and sqrt.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB_DIR = PKG / "lib"
+LIB = LIB_DIR / "libvc3_b200.so"
+SOURCES = ["vc3_kernels.cu", "vc3_host.cu"]
+HEADERS = ["vc3_device.cuh"]
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NUMERICS = ["-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found; set NVCC or install the CUDA toolkit")
+
+
+def _stale() -> bool:
+    if not LIB.exists():
+        return True
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "vc3_b200.h", Path(__file__)]
+    built = LIB.stat().st_mtime
+    return any(d.stat().st_mtime > built for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile the shared library if any source is newer than it."""
+    if not force and not _stale():
+        return LIB
+    LIB_DIR.mkdir(exist_ok=True)
+    tmp = LIB.with_suffix(".so.tmp")
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", *NUMERICS,
+           "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
+           "-I", str(ROOT / "include"),
+           *(str(CSRC / s) for s in SOURCES), "-o", str(tmp)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+        print(" ".join(cmd))
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+TOOLS = ROOT / "tools"
+
+
+def build_exhaustive(force: bool = False) -> Path:
+    """The FMA-equivalence enumerator (test infrastructure, tools/exhaustive.cu)."""
+    out = TOOLS / "exhaustive"
+    src = TOOLS / "exhaustive.cu"
+    deps = [src, CSRC / "vc3_device.cuh"]
+    if force or not out.exists() or any(d.stat().st_mtime > out.stat().st_mtime for d in deps):
+        subprocess.run([nvcc(), *ARCH, "-O3", "-std=c++17", *NUMERICS, "-I", str(ROOT / "include"),
+                        str(src), "-o", str(out)], check=True)
+    return out
+
+
+if __name__ == "__main__":
+    import sys
+
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,204 @@
+"""Input domains and round-trip error statistics on the GPU path.
+
+* ``SampleDomain`` / ``sample`` restate the reference's deterministic
+  generator (/root/reference/pkg/src/vc3/analysis.py:34-99): chunk ``i`` of
+  ``CHUNK`` vectors is drawn from numpy ``Philox(key=(seed, i))``, so every
+  input the reference studies can be reproduced bit for bit here.
+* ``error_study`` (analysis.py:157-167) runs compress -> decompress -> the
+  K6 per-chunk moment kernel on the device and merges chunk moments on the
+  host in chunk order with the reference's merge formula (analysis.py:118-145).
+* ``error_study_sharded`` splits the chunks over the ranks of a
+  ``torch.distributed`` group (contiguous blocks of chunks, no data-path
+  collective) and all-gathers the 32-byte per-chunk tuples; the merge in
+  global chunk order makes the result identical on every rank and identical
+  to the single-process result.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _dev, _native
+from ._dev import torch
+from .codec import compress, decompress
+from .errors import EmptyDomain
+from .layout import DEFAULT_LAYOUT, DEFAULT_POLICY, as_layout, as_policy
+
+CHUNK = 1 << 20   # analysis.py:29
+
+_KINDS = ("unit_sphere", "sphere_angles", "cube", "shell")
+
+
+@dataclass(frozen=True)
+class SampleDomain:
+    """Region, count and seed of a deterministic float32 sample stream."""
+
+    kind: str = "unit_sphere"
+    count: int = 1_000_000
+    seed: int = 0
+    r_min: float = 1.0
+    r_max: float = 1.0
+
+    def __post_init__(self):
+        if self.kind not in _KINDS:
+            raise ValueError(f"unknown domain kind {self.kind!r}")
+        if self.count < 0:
+            raise ValueError("count must be non-negative")
+        if self.kind == "shell" and not 0 <= self.r_min <= self.r_max:
+            raise ValueError("shell needs 0 <= r_min <= r_max")
+
+    def describe(self) -> str:
+        return f"shell:{self.r_min:g}:{self.r_max:g}" if self.kind == "shell" else self.kind
+
+    def chunk(self, index: int, n: int) -> np.ndarray:
+        """Chunk ``index`` (``n`` vectors); draws in the reference's order."""
+        rng = np.random.Generator(np.random.Philox(key=(self.seed, index)))
+        if self.kind == "cube":
+            return rng.uniform(-1.0, 1.0, (n, 3)).astype(np.float32)
+        if self.kind == "sphere_angles":
+            theta = rng.uniform(-np.pi, np.pi, n)
+            phi = rng.uniform(0.0, np.pi, n)
+            sin_phi = np.sin(phi)
+            out = np.stack([sin_phi * np.cos(theta), sin_phi * np.sin(theta), np.cos(phi)], axis=1)
+            return out.astype(np.float32)
+        theta = rng.uniform(-np.pi, np.pi, n)
+        z = rng.uniform(-1.0, 1.0, n)
+        ring = np.sqrt(1.0 - z * z)
+        out = np.stack([ring * np.cos(theta), ring * np.sin(theta), z], axis=1)
+        if self.kind == "shell":
+            out = out * rng.uniform(self.r_min, self.r_max, n)[:, None]
+        return out.astype(np.float32)
+
+    def n_chunks(self) -> int:
+        return (self.count + CHUNK - 1) // CHUNK
+
+    def chunk_size(self, index: int) -> int:
+        return min(CHUNK, self.count - index * CHUNK)
+
+    def chunks(self):
+        for i in range(self.n_chunks()):
+            yield self.chunk(i, self.chunk_size(i))
+
+
+def sample(domain: SampleDomain) -> np.ndarray:
+    """Whole (count, 3) float32 sample (analysis.py:93-97)."""
+    if domain.count == 0:
+        return np.empty((0, 3), dtype=np.float32)
+    return np.concatenate(list(domain.chunks()), axis=0)
+
+
+@dataclass
+class ErrorStats:
+    mean: float
+    max: float
+    stddev: float
+    count: int
+    normalised: bool
+
+    def to_dict(self) -> dict:
+        return {"mean": self.mean, "max": self.max, "stddev": self.stddev,
+                "count": self.count, "normalised": self.normalised}
+
+
+class ChunkMerger:
+    """Merge per-chunk (count, mean, M2, max) in chunk order with the
+    reference's update rule (analysis.py:127-141)."""
+
+    def __init__(self):
+        self.n = 0
+        self.mean = 0.0
+        self.m2 = 0.0
+        self.max = 0.0
+
+    def add(self, count: int, mean: float, m2: float, mx: float):
+        if count == 0:
+            return
+        if self.n == 0:
+            self.n, self.mean, self.m2 = count, mean, m2
+        else:
+            n = self.n + count
+            d = mean - self.mean
+            self.mean += d * count / n
+            self.m2 += m2 + d * d * self.n * count / n
+            self.n = n
+        self.max = max(self.max, mx)
+
+    def stats(self, normalised: bool) -> ErrorStats:
+        sd = math.sqrt(self.m2 / (self.n - 1)) if self.n > 1 else 0.0
+        return ErrorStats(self.mean, self.max, sd, self.n, normalised)
+
+
+def chunk_moments(v, vh, normalised: bool, chunk: int = CHUNK):
+    """Device K6 kernel: (k, 4) float64 tensor of per-chunk moments of
+    e = ||v - vh||_2 (optionally / ||v||) for CUDA tensors v, vh of shape (n, 3)."""
+    lib = _native.load()
+    n = v.shape[0]
+    k = max(1, (n + chunk - 1) // chunk)
+    out = torch.zeros((k, 4), dtype=torch.float64, device=v.device)
+    _native.check(lib.vc3_error_stats(v.data_ptr(), vh.data_ptr(), n, int(bool(normalised)),
+                                      chunk, out.data_ptr(), _dev.stream_of(v)), "error_stats")
+    return out
+
+
+def _chunk_tuple(domain: SampleDomain, index: int, layout, policy, normalised: bool) -> np.ndarray:
+    v = _dev.upload(domain.chunk(index, domain.chunk_size(index)))
+    vh = decompress(compress(v, layout, policy), layout)
+    return chunk_moments(v, vh, normalised, CHUNK)[0].cpu().numpy()
+
+
+def error_study(domain: SampleDomain, layout=DEFAULT_LAYOUT, policy=DEFAULT_POLICY,
+                normalised: bool = False) -> ErrorStats:
+    """Round-trip L2 error statistics over a sample domain (analysis.py:157-167)."""
+    if domain.count == 0:
+        raise EmptyDomain("error_study needs at least one sample")
+    layout, policy = as_layout(layout), as_policy(policy)
+    acc = ChunkMerger()
+    for i in range(domain.n_chunks()):
+        c = _chunk_tuple(domain, i, layout, policy, normalised)
+        acc.add(int(c[0]), float(c[1]), float(c[2]), float(c[3]))
+    return acc.stats(normalised)
+
+
+def shard_range(n_items: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous block [lo, hi) of ``n_items`` owned by ``rank`` (ceil split)."""
+    per = (n_items + world - 1) // world
+    lo = min(n_items, rank * per)
+    return lo, min(n_items, lo + per)
+
+
+def error_study_sharded(domain: SampleDomain, layout=DEFAULT_LAYOUT, policy=DEFAULT_POLICY,
+                        normalised: bool = False, group=None,
+                        tuple_fn=None) -> ErrorStats:
+    """``error_study`` with chunks split over a torch.distributed group.
+
+    The only exchange is an all-gather of the (count, mean, M2, max) tuples
+    (32 B per chunk); NCCL when the group's backend is nccl, gloo on CPU.
+    ``tuple_fn(domain, index)`` overrides the per-chunk computation (tests use
+    it to exercise the host logic without a GPU)."""
+    import torch.distributed as dist
+
+    if domain.count == 0:
+        raise EmptyDomain("error_study needs at least one sample")
+    layout, policy = as_layout(layout), as_policy(policy)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    nch = domain.n_chunks()
+    per = (nch + world - 1) // world
+    lo, hi = shard_range(nch, rank, world)
+    fn = tuple_fn or (lambda d, i: _chunk_tuple(d, i, layout, policy, normalised))
+    mine = np.zeros((per, 4), dtype=np.float64)
+    for j, i in enumerate(range(lo, hi)):
+        mine[j] = fn(domain, i)
+    backend = dist.get_backend(group)
+    dev = (torch.device("cuda", torch.cuda.current_device()) if backend == "nccl"
+           else torch.device("cpu"))
+    local = torch.from_numpy(mine).to(dev)
+    gathered = [torch.empty_like(local) for _ in range(world)]
+    dist.all_gather(gathered, local, group=group)
+    table = torch.cat(gathered).cpu().numpy()[:nch]
+    acc = ChunkMerger()
+    for row in table:
+        acc.add(int(row[0]), float(row[1]), float(row[2]), float(row[3]))
+    return acc.stats(normalised)

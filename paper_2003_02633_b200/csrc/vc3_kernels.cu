@@ -1,0 +1,708 @@
+// vc3_kernels.cu — sm_100a kernels of the inline 3-vector codec and the
+// extern "C" boundary declared in include/vc3_b200.h.
+//
+// Memory layout in HBM: compressed words are contiguous uint64
+// arrays moved as 16-byte ulonglong2 pairs; vectors are the caller's
+// array-of-structs float32 [n][3] moved as three 16-byte float4 per group of
+// four vectors.  Every kernel is a grid-stride streaming loop sized to a
+// multiple of the 148 SMs; nothing is staged through an uncompressed HBM
+// intermediate.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <mutex>
+
+#include "../../include/vc3_b200.h"
+#include "vc3_device.cuh"
+
+using namespace vc3;
+
+#ifndef VC3_USE_FMA
+// Fused Horner / bucket FMAs: enabled after tools/exhaustive.cu proved them
+// bit-identical to the reference's unfused sequence over every float32 input.
+#define VC3_USE_FMA 1
+#endif
+constexpr bool kFma = VC3_USE_FMA != 0;
+
+namespace {
+
+thread_local int g_last_cuda = 0;
+
+int cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return VC3_OK;
+    g_last_cuda = (int)e;
+    return VC3_ERR_CUDA;
+}
+
+int launch_status() { return cuda_status(cudaGetLastError()); }
+
+int sm_count() {
+    static int count = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            count = 148;
+    });
+    return count;
+}
+
+constexpr int kThreads = 256;
+
+// grid for `items` work items of one thread each: at most 8 resident CTAs per SM
+// worth of blocks (grid-stride beyond that), at least one.
+unsigned grid_for(int64_t items, int per_sm = 8) {
+    int64_t blocks = (items + kThreads - 1) / kThreads;
+    int64_t cap = (int64_t)sm_count() * per_sm;
+    if (blocks > cap) blocks = cap;
+    return (unsigned)(blocks < 1 ? 1 : blocks);
+}
+
+bool layout_ok(const vc3_layout& L) {
+    const int s = L.sign_bits, e = L.exponent_bits, m = L.mantissa_bits, p = L.phi_bits,
+              t = L.theta_bits;
+    if (s != 0 && s != 1) return false;
+    if (e < 1 || e > 8 || m < 1 || m > 23 || p < 1 || p > 32 || t < 1 || t > 32) return false;
+    if (s + e + m + p + t != 64) return false;
+    if (e == 8 && L.exponent_bias != 127) return false;
+    if (L.exponent_bias < 0 || L.exponent_bias > 128) return false;
+    return true;
+}
+
+// Host derivation of the by-value parameter block.  The double expressions
+// are the reference's (_kernels.py:139-140) evaluated in IEEE double.
+Params make_params(const vc3_layout& L) {
+    Params P;
+    P.e = L.exponent_bits;
+    P.m = L.mantissa_bits;
+    P.p = L.phi_bits;
+    P.t = L.theta_bits;
+    P.bias = L.exponent_bias;
+    P.emax = (1 << P.e) - 1;
+    P.ntmax = (1LL << P.t) - 1;
+    P.npmax = (1LL << P.p) - 1;
+    P.tmask = (unsigned long long)P.ntmax;
+    P.pmask = (unsigned long long)P.npmax;
+    const volatile double pi = kPi;  // keep host arithmetic plain IEEE double
+    P.nt_half = (double)P.ntmax / 2.0;
+    P.t_scale = (double)P.ntmax / (2.0 * pi);
+    P.p_scale = (double)P.npmax / pi;
+    P.t_step = pi / (2.0 * (double)P.ntmax);
+    P.p_step = pi / (2.0 * (double)P.npmax);
+    P.field_low = 2u << P.m;
+    P.field_high = ((unsigned)(P.emax - 1) << P.m) | ((1u << P.m) - 1u);
+    return P;
+}
+
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+// ----- streaming loads/stores (read-once data: keep it out of L1) ----------
+__device__ __forceinline__ ulonglong2 ld_stream_u2(const unsigned long long* p) {
+    ulonglong2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(v.x), "=l"(v.y)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_u2(unsigned long long* p, unsigned long long a,
+                                      unsigned long long b) {
+    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void st_f4(float* p, float a, float b, float c, float d) {
+    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ int64_t gtid() {
+    return (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+}
+__device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
+
+// ===================== kernels ==============================================
+
+// K1 compress: 4 vectors (48 B in, 32 B out) per thread per step.
+template <unsigned POLICY, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_compress(const float* __restrict__ xyz,
+                                                       unsigned long long* __restrict__ out,
+                                                       int64_t n, Params P,
+                                                       int32_t* __restrict__ nonfinite) {
+    int bad = 0;
+    const int64_t groups = VEC ? n / 4 : 0;
+    for (int64_t g = gtid(); g < groups; g += gstride()) {
+        const float* src = xyz + 12 * g;
+        const float4 a = ld_stream_f4(src), b = ld_stream_f4(src + 4), c = ld_stream_f4(src + 8);
+        bad += !finite3(a.x, a.y, a.z) + !finite3(a.w, b.x, b.y) + !finite3(b.z, b.w, c.x) +
+               !finite3(c.y, c.z, c.w);
+        const unsigned long long w0 = compress_one<POLICY, kFma>(a.x, a.y, a.z, P);
+        const unsigned long long w1 = compress_one<POLICY, kFma>(a.w, b.x, b.y, P);
+        const unsigned long long w2 = compress_one<POLICY, kFma>(b.z, b.w, c.x, P);
+        const unsigned long long w3 = compress_one<POLICY, kFma>(c.y, c.z, c.w, P);
+        st_u2(out + 4 * g, w0, w1);
+        st_u2(out + 4 * g + 2, w2, w3);
+    }
+    for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
+        const float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+        bad += !finite3(x, y, z);
+        out[i] = compress_one<POLICY, kFma>(x, y, z, P);
+    }
+    if (bad && nonfinite) atomicAdd(nonfinite, bad);
+}
+
+// K2 decompress: 4 words (32 B in, 48 B out) per thread per step.
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_decompress(const unsigned long long* __restrict__ w,
+                                                         float* __restrict__ xyz, int64_t n,
+                                                         Params P) {
+    const int64_t groups = VEC ? n / 4 : 0;
+    for (int64_t g = gtid(); g < groups; g += gstride()) {
+        const ulonglong2 u = ld_stream_u2(w + 4 * g), v = ld_stream_u2(w + 4 * g + 2);
+        float o[12];
+        decompress_one(u.x, P, o[0], o[1], o[2]);
+        decompress_one(u.y, P, o[3], o[4], o[5]);
+        decompress_one(v.x, P, o[6], o[7], o[8]);
+        decompress_one(v.y, P, o[9], o[10], o[11]);
+        float* dst = xyz + 12 * g;
+        st_f4(dst, o[0], o[1], o[2], o[3]);
+        st_f4(dst + 4, o[4], o[5], o[6], o[7]);
+        st_f4(dst + 8, o[8], o[9], o[10], o[11]);
+    }
+    for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
+        float x, y, z;
+        decompress_one(w[i], P, x, y, z);
+        xyz[3 * i] = x;
+        xyz[3 * i + 1] = y;
+        xyz[3 * i + 2] = z;
+    }
+}
+
+// K3 fused add: c = compress(decompress(a) + decompress(b)) (_kernels.py:348-359)
+template <unsigned POLICY>
+__device__ __forceinline__ unsigned long long add_one(unsigned long long a, unsigned long long b,
+                                                      const Params& P) {
+    float x1, y1, z1, x2, y2, z2;
+    decompress_one(a, P, x1, y1, z1);
+    decompress_one(b, P, x2, y2, z2);
+    return compress_one<POLICY, kFma>(__fadd_rn(x1, x2), __fadd_rn(y1, y2), __fadd_rn(z1, z2), P);
+}
+
+template <unsigned POLICY, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_add(const unsigned long long* __restrict__ a,
+                                                  const unsigned long long* __restrict__ b,
+                                                  unsigned long long* __restrict__ c, int64_t n,
+                                                  Params P) {
+    const int64_t pairs = VEC ? n / 2 : 0;
+    for (int64_t g = gtid(); g < pairs; g += gstride()) {
+        const ulonglong2 u = ld_stream_u2(a + 2 * g), v = ld_stream_u2(b + 2 * g);
+        st_u2(c + 2 * g, add_one<POLICY>(u.x, v.x, P), add_one<POLICY>(u.y, v.y, P));
+    }
+    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride()) c[i] = add_one<POLICY>(a[i], b[i], P);
+}
+
+// K5 uncompressed baseline: flat float32 add (_kernels.py:341-345)
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) k_add_raw(const float* __restrict__ a,
+                                                      const float* __restrict__ b,
+                                                      float* __restrict__ c, int64_t n) {
+    const int64_t quads = VEC ? n / 4 : 0;
+    for (int64_t g = gtid(); g < quads; g += gstride()) {
+        const float4 u = ld_stream_f4(a + 4 * g), v = ld_stream_f4(b + 4 * g);
+        st_f4(c + 4 * g, __fadd_rn(u.x, v.x), __fadd_rn(u.y, v.y), __fadd_rn(u.z, v.z),
+              __fadd_rn(u.w, v.w));
+    }
+    for (int64_t i = quads * 4 + gtid(); i < n; i += gstride()) c[i] = __fadd_rn(a[i], b[i]);
+}
+
+// K4 axpy: y' = compress(alpha*decode(x) + decode(y))
+template <unsigned POLICY>
+__device__ __forceinline__ unsigned long long axpy_one(float al, unsigned long long x,
+                                                       unsigned long long y, const Params& P) {
+    float x1, y1, z1, x2, y2, z2;
+    decompress_one(x, P, x1, y1, z1);
+    decompress_one(y, P, x2, y2, z2);
+    return compress_one<POLICY, kFma>(__fadd_rn(__fmul_rn(al, x1), x2),
+                                      __fadd_rn(__fmul_rn(al, y1), y2),
+                                      __fadd_rn(__fmul_rn(al, z1), z2), P);
+}
+
+template <unsigned POLICY, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_axpy(float al, const unsigned long long* __restrict__ x,
+                                                   const unsigned long long* y,
+                                                   unsigned long long* yo, int64_t n, Params P) {
+    const int64_t pairs = VEC ? n / 2 : 0;
+    for (int64_t g = gtid(); g < pairs; g += gstride()) {
+        const ulonglong2 u = ld_stream_u2(x + 2 * g);
+        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(y + 2 * g);  // may alias yo
+        st_u2(yo + 2 * g, axpy_one<POLICY>(al, u.x, v.x, P), axpy_one<POLICY>(al, u.y, v.y, P));
+    }
+    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride()) yo[i] = axpy_one<POLICY>(al, x[i], y[i], P);
+}
+
+// K4b low-storage RK stage: dq' = a*dq + dt*R ; q' = q + b*dq'
+template <unsigned POLICY>
+__device__ __forceinline__ void rk_one(float ca, float cb, float dt, unsigned long long& q,
+                                       unsigned long long& dq, unsigned long long r,
+                                       const Params& P) {
+    float q0, q1, q2, d0, d1, d2, r0, r1, r2;
+    decompress_one(q, P, q0, q1, q2);
+    decompress_one(dq, P, d0, d1, d2);
+    decompress_one(r, P, r0, r1, r2);
+    d0 = __fadd_rn(__fmul_rn(ca, d0), __fmul_rn(dt, r0));
+    d1 = __fadd_rn(__fmul_rn(ca, d1), __fmul_rn(dt, r1));
+    d2 = __fadd_rn(__fmul_rn(ca, d2), __fmul_rn(dt, r2));
+    q0 = __fadd_rn(q0, __fmul_rn(cb, d0));
+    q1 = __fadd_rn(q1, __fmul_rn(cb, d1));
+    q2 = __fadd_rn(q2, __fmul_rn(cb, d2));
+    dq = compress_one<POLICY, kFma>(d0, d1, d2, P);
+    q = compress_one<POLICY, kFma>(q0, q1, q2, P);
+}
+
+template <unsigned POLICY, bool VEC>
+__global__ void __launch_bounds__(kThreads) k_rk(float ca, float cb, float dt,
+                                                 unsigned long long* __restrict__ q,
+                                                 unsigned long long* __restrict__ dq,
+                                                 const unsigned long long* __restrict__ R,
+                                                 int64_t n, Params P) {
+    const int64_t pairs = VEC ? n / 2 : 0;
+    for (int64_t g = gtid(); g < pairs; g += gstride()) {
+        ulonglong2 u = *reinterpret_cast<const ulonglong2*>(q + 2 * g);
+        ulonglong2 v = *reinterpret_cast<const ulonglong2*>(dq + 2 * g);
+        const ulonglong2 r = ld_stream_u2(R + 2 * g);
+        rk_one<POLICY>(ca, cb, dt, u.x, v.x, r.x, P);
+        rk_one<POLICY>(ca, cb, dt, u.y, v.y, r.y, P);
+        st_u2(q + 2 * g, u.x, u.y);
+        st_u2(dq + 2 * g, v.x, v.y);
+    }
+    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride()) {
+        unsigned long long qq = q[i], dd = dq[i];
+        rk_one<POLICY>(ca, cb, dt, qq, dd, R[i], P);
+        q[i] = qq;
+        dq[i] = dd;
+    }
+}
+
+// ----- pieces ----------------------------------------------------------------
+template <unsigned POLICY>
+__global__ void __launch_bounds__(kThreads) k_spherical(const float* __restrict__ xyz,
+                                                        double* __restrict__ r,
+                                                        double* __restrict__ th,
+                                                        double* __restrict__ ph, int64_t n,
+                                                        int32_t* nonfinite) {
+    constexpr bool TS = POLICY & kThetaSingle, PS = POLICY & kPhiSingle;
+    int bad = 0;
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        const float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+        bad += !finite3(x, y, z);
+        const double xd = x, yd = y, zd = z;
+        const double s = __fma_rn(zd, zd, __fma_rn(yd, yd, __dmul_rn(xd, xd)));
+        double rr = 0.0, t = 0.0, p = 0.0;
+        if (s != 0.0) {
+            rr = __dsqrt_rn(s);
+            t = TS ? (double)atan2_f32<kFma>(y, x) : atan2(yd, xd);
+            if (PS) {
+                const float sq =
+                    __fadd_rn(__fadd_rn(__fmul_rn(x, x), __fmul_rn(y, y)), __fmul_rn(z, z));
+                const float rq = __fsqrt_rn(sq);
+                float w = 1.0f;
+                if (rq > 0.0f) w = fminf(fmaxf(__fdiv_rn(z, rq), -1.0f), 1.0f);
+                p = (double)acos_f32<kFma>(w);
+            } else {
+                p = acos(fmin(fmax(__ddiv_rn(zd, rr), -1.0), 1.0));
+            }
+        }
+        r[i] = rr;
+        th[i] = t;
+        ph[i] = p;
+    }
+    if (bad && nonfinite) atomicAdd(nonfinite, bad);
+}
+
+__global__ void __launch_bounds__(kThreads) k_quantize(const double* __restrict__ th,
+                                                       const double* __restrict__ ph,
+                                                       long long* __restrict__ nt,
+                                                       long long* __restrict__ nph, int64_t n,
+                                                       Params P, int quant_single) {
+    // Arbitrary caller angles: the unfused reference sequence (no FMA proof applies).
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        long long a, b;
+        quantize<false>(th[i], ph[i], quant_single != 0, P, a, b);
+        nt[i] = a;
+        nph[i] = b;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_dequantize(const long long* __restrict__ nt,
+                                                         const long long* __restrict__ nph,
+                                                         double* __restrict__ th,
+                                                         double* __restrict__ ph, int64_t n,
+                                                         Params P) {
+    // dequantize_kernel (_kernels.py:334-338): pi*(2n/nmax - 1), pi*n/nmax
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        th[i] = __dmul_rn(kPi, __dsub_rn(__ddiv_rn(__dmul_rn(2.0, (double)nt[i]), (double)P.ntmax), 1.0));
+        ph[i] = __ddiv_rn(__dmul_rn(kPi, (double)nph[i]), (double)P.npmax);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_encode_mag(const double* __restrict__ r,
+                                                         unsigned long long* __restrict__ f,
+                                                         int64_t n, Params P) {
+    for (int64_t i = gtid(); i < n; i += gstride()) f[i] = encode_mag(r[i], P);
+}
+
+__global__ void __launch_bounds__(kThreads) k_decode_mag(const long long* __restrict__ f,
+                                                         float* __restrict__ r, int64_t n,
+                                                         Params P) {
+    for (int64_t i = gtid(); i < n; i += gstride()) r[i] = decode_mag((unsigned long long)f[i], P);
+}
+
+__global__ void __launch_bounds__(kThreads) k_mag_events(const float* __restrict__ xyz, int64_t n,
+                                                         Params P,
+                                                         unsigned long long* __restrict__ counts) {
+    unsigned long long fl = 0, sat = 0;
+    for (int64_t i = gtid(); i < n; i += gstride()) {
+        const double xd = xyz[3 * i], yd = xyz[3 * i + 1], zd = xyz[3 * i + 2];
+        const double r = __dsqrt_rn(__fma_rn(zd, zd, __fma_rn(yd, yd, __dmul_rn(xd, xd))));
+        if (r > 0.0) {
+            const unsigned u = __float_as_uint(__double2float_ru(r));
+            const int e7 = (int)((u >> 23) & 0xFFu) - 127 + P.bias;
+            fl += e7 <= 1;
+            sat += e7 >= P.emax;
+        }
+    }
+    if (fl) atomicAdd(counts, fl);
+    if (sat) atomicAdd(counts + 1, sat);
+}
+
+// ----- K6 error statistics (analysis.py:118-167) ------------------------------
+// Stage 1: each block reduces a contiguous slice of one chunk to (n, mean, M2, max)
+// with per-thread Welford and Chan merges in a fixed order (deterministic).
+struct Moments {
+    double n, mean, m2, max;
+};
+
+__device__ __forceinline__ Moments chan(Moments a, Moments b) {
+    if (a.n == 0) return b;
+    if (b.n == 0) return a;
+    const double n = a.n + b.n, d = b.mean - a.mean;
+    Moments r;
+    r.n = n;
+    r.mean = a.mean + d * (b.n / n);
+    r.m2 = a.m2 + b.m2 + d * d * (a.n * b.n / n);
+    r.max = fmax(a.max, b.max);
+    return r;
+}
+
+__device__ __forceinline__ double err_one(const float* v, const float* vh, int64_t i, int normalised) {
+    const double dx = (double)v[3 * i] - (double)vh[3 * i];
+    const double dy = (double)v[3 * i + 1] - (double)vh[3 * i + 1];
+    const double dz = (double)v[3 * i + 2] - (double)vh[3 * i + 2];
+    double e = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
+    if (normalised) {
+        const double x = v[3 * i], y = v[3 * i + 1], z = v[3 * i + 2];
+        const double nv = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+        e = __ddiv_rn(e, nv > 0.0 ? nv : 1.0);
+    }
+    return e;
+}
+
+constexpr int kStatThreads = 256;
+constexpr int kStatSlice = 8192;  // vectors per block slice
+
+__global__ void __launch_bounds__(kStatThreads) k_err_partial(const float* __restrict__ v,
+                                                              const float* __restrict__ vh,
+                                                              int64_t n, int normalised,
+                                                              int64_t chunk, int slices_per_chunk,
+                                                              Moments* __restrict__ part) {
+    const int64_t c = blockIdx.y, s = blockIdx.x;
+    const int64_t c0 = c * chunk, c1 = min(n, c0 + chunk);
+    const int64_t lo = c0 + s * (int64_t)kStatSlice, hi = min(c1, lo + kStatSlice);
+    Moments m = {0, 0, 0, 0};
+    for (int64_t i = lo + threadIdx.x; i < hi; i += kStatThreads) {
+        const double e = err_one(v, vh, i, normalised);
+        m.n += 1;
+        const double d = e - m.mean;
+        m.mean += d / m.n;
+        m.m2 += d * (e - m.mean);
+        m.max = fmax(m.max, e);
+    }
+    __shared__ Moments sh[kStatThreads];
+    sh[threadIdx.x] = m;
+    __syncthreads();
+    for (int w = kStatThreads / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) sh[threadIdx.x] = chan(sh[threadIdx.x], sh[threadIdx.x + w]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[c * slices_per_chunk + s] = sh[0];
+}
+
+__global__ void k_err_final(const Moments* __restrict__ part, int64_t nchunks,
+                            int slices_per_chunk, double* __restrict__ out) {
+    for (int64_t c = gtid(); c < nchunks; c += gstride()) {
+        Moments m = {0, 0, 0, 0};
+        for (int s = 0; s < slices_per_chunk; ++s) m = chan(m, part[c * slices_per_chunk + s]);
+        out[4 * c] = m.n;
+        out[4 * c + 1] = m.mean;
+        out[4 * c + 2] = m.m2;
+        out[4 * c + 3] = m.max;
+    }
+}
+
+// ----- dispatch helpers ----------------------------------------------------------
+template <template <unsigned> class F, typename... A>
+int by_policy(uint32_t pol, A... args) {
+    switch (pol & 7u) {
+        case 0: return F<0>::run(args...);
+        case 1: return F<1>::run(args...);
+        case 2: return F<2>::run(args...);
+        case 3: return F<3>::run(args...);
+        case 4: return F<4>::run(args...);
+        case 5: return F<5>::run(args...);
+        case 6: return F<6>::run(args...);
+        default: return F<7>::run(args...);
+    }
+}
+
+template <unsigned POL>
+struct RunCompress {
+    static int run(const float* x, uint64_t* w, int64_t n, const Params& P, int32_t* nf, cudaStream_t s) {
+        if (aligned16(x) && aligned16(w)) {
+            k_compress<POL, true><<<grid_for((n + 3) / 4), kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, nf);
+        } else {
+            k_compress<POL, false><<<grid_for(n), kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, nf);
+        }
+        return launch_status();
+    }
+};
+
+template <unsigned POL>
+struct RunAdd {
+    static int run(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t n, const Params& P,
+                   cudaStream_t s) {
+        auto A = (const unsigned long long*)a, B = (const unsigned long long*)b;
+        auto C = (unsigned long long*)c;
+        if (aligned16(a) && aligned16(b) && aligned16(c))
+            k_add<POL, true><<<grid_for((n + 1) / 2), kThreads, 0, s>>>(A, B, C, n, P);
+        else
+            k_add<POL, false><<<grid_for(n), kThreads, 0, s>>>(A, B, C, n, P);
+        return launch_status();
+    }
+};
+
+template <unsigned POL>
+struct RunAxpy {
+    static int run(float al, const uint64_t* x, const uint64_t* y, uint64_t* yo, int64_t n,
+                   const Params& P, cudaStream_t s) {
+        auto X = (const unsigned long long*)x, Y = (const unsigned long long*)y;
+        auto O = (unsigned long long*)yo;
+        if (aligned16(x) && aligned16(y) && aligned16(yo))
+            k_axpy<POL, true><<<grid_for((n + 1) / 2), kThreads, 0, s>>>(al, X, Y, O, n, P);
+        else
+            k_axpy<POL, false><<<grid_for(n), kThreads, 0, s>>>(al, X, Y, O, n, P);
+        return launch_status();
+    }
+};
+
+template <unsigned POL>
+struct RunRk {
+    static int run(float ca, float cb, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
+                   int64_t n, const Params& P, cudaStream_t s) {
+        auto Q = (unsigned long long*)q, D = (unsigned long long*)dq;
+        auto RR = (const unsigned long long*)R;
+        if (aligned16(q) && aligned16(dq) && aligned16(R))
+            k_rk<POL, true><<<grid_for((n + 1) / 2), kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P);
+        else
+            k_rk<POL, false><<<grid_for(n), kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P);
+        return launch_status();
+    }
+};
+
+template <unsigned POL>
+struct RunSpherical {
+    static int run(const float* x, double* r, double* t, double* p, int64_t n, int32_t* nf,
+                   cudaStream_t s) {
+        k_spherical<POL & 3u><<<grid_for(n), kThreads, 0, s>>>(x, r, t, p, n, nf);
+        return launch_status();
+    }
+};
+
+#define VC3_CHECK_N(n) \
+    if ((n) < 0) return VC3_ERR_ARG; \
+    if ((n) == 0) return VC3_OK;
+
+}  // namespace
+
+// ===================== extern "C" boundary ====================================
+extern "C" {
+
+const char* vc3_version(void) { return "vc3-b200 0.1.0 (sm_100a)"; }
+
+const char* vc3_status_string(int status) {
+    switch (status) {
+        case VC3_OK: return "ok";
+        case VC3_ERR_LAYOUT: return "invalid bit layout";
+        case VC3_ERR_ARG: return "invalid argument";
+        case VC3_ERR_CUDA: return "CUDA error";
+        case VC3_ERR_NONFINITE: return "non-finite input";
+        case VC3_ERR_LENGTH: return "length mismatch";
+        default: return "unknown status";
+    }
+}
+
+int vc3_last_cuda_error(void) { return g_last_cuda; }
+
+int vc3_validate_layout(vc3_layout layout) { return layout_ok(layout) ? VC3_OK : VC3_ERR_LAYOUT; }
+
+int vc3_compress(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout, uint32_t policy,
+                 int32_t* d_nonfinite, void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    if (policy > 7u) return VC3_ERR_ARG;
+    VC3_CHECK_N(n);
+    if (!xyz || !words) return VC3_ERR_ARG;
+    return by_policy<RunCompress>(policy, xyz, words, n, make_params(layout), d_nonfinite,
+                                  (cudaStream_t)stream);
+}
+
+int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout, void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    VC3_CHECK_N(n);
+    if (!xyz || !words) return VC3_ERR_ARG;
+    const Params P = make_params(layout);
+    auto W = (const unsigned long long*)words;
+    if (aligned16(words) && aligned16(xyz))
+        k_decompress<true><<<grid_for((n + 3) / 4), kThreads, 0, (cudaStream_t)stream>>>(W, xyz, n, P);
+    else
+        k_decompress<false><<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(W, xyz, n, P);
+    return launch_status();
+}
+
+int vc3_add_compressed(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t n,
+                       vc3_layout layout, uint32_t policy, void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    if (policy > 7u) return VC3_ERR_ARG;
+    VC3_CHECK_N(n);
+    if (!a || !b || !c) return VC3_ERR_ARG;
+    return by_policy<RunAdd>(policy, a, b, c, n, make_params(layout), (cudaStream_t)stream);
+}
+
+int vc3_add_raw(const float* a, const float* b, float* c, int64_t n_floats, void* stream) {
+    VC3_CHECK_N(n_floats);
+    if (!a || !b || !c) return VC3_ERR_ARG;
+    if (aligned16(a) && aligned16(b) && aligned16(c))
+        k_add_raw<true><<<grid_for((n_floats + 3) / 4), kThreads, 0, (cudaStream_t)stream>>>(a, b, c, n_floats);
+    else
+        k_add_raw<false><<<grid_for(n_floats), kThreads, 0, (cudaStream_t)stream>>>(a, b, c, n_floats);
+    return launch_status();
+}
+
+int vc3_axpy(float alpha, const uint64_t* x, const uint64_t* y, uint64_t* y_out, int64_t n,
+             vc3_layout layout, uint32_t policy, void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    if (policy > 7u) return VC3_ERR_ARG;
+    VC3_CHECK_N(n);
+    if (!x || !y || !y_out) return VC3_ERR_ARG;
+    return by_policy<RunAxpy>(policy, alpha, x, y, y_out, n, make_params(layout),
+                              (cudaStream_t)stream);
+}
+
+int vc3_rk_stage(float a, float b, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
+                 int64_t n, vc3_layout layout, uint32_t policy, void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    if (policy > 7u) return VC3_ERR_ARG;
+    VC3_CHECK_N(n);
+    if (!q || !dq || !R) return VC3_ERR_ARG;
+    return by_policy<RunRk>(policy, a, b, dt, q, dq, R, n, make_params(layout),
+                            (cudaStream_t)stream);
+}
+
+int vc3_to_spherical(const float* xyz, double* r, double* theta, double* phi, int64_t n,
+                     uint32_t policy, int32_t* d_nonfinite, void* stream) {
+    if (policy > 7u) return VC3_ERR_ARG;
+    VC3_CHECK_N(n);
+    if (!xyz || !r || !theta || !phi) return VC3_ERR_ARG;
+    return by_policy<RunSpherical>(policy, xyz, r, theta, phi, n, d_nonfinite,
+                                   (cudaStream_t)stream);
+}
+
+int vc3_quantize_angles(const double* theta, const double* phi, int64_t* n_theta, int64_t* n_phi,
+                        int64_t n, vc3_layout layout, uint32_t policy, void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    if (policy > 7u) return VC3_ERR_ARG;
+    VC3_CHECK_N(n);
+    if (!theta || !phi || !n_theta || !n_phi) return VC3_ERR_ARG;
+    k_quantize<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(
+        theta, phi, (long long*)n_theta, (long long*)n_phi, n, make_params(layout),
+        (policy & VC3_QUANT_SINGLE) ? 1 : 0);
+    return launch_status();
+}
+
+int vc3_dequantize_angles(const int64_t* n_theta, const int64_t* n_phi, double* theta, double* phi,
+                          int64_t n, vc3_layout layout, void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    VC3_CHECK_N(n);
+    if (!theta || !phi || !n_theta || !n_phi) return VC3_ERR_ARG;
+    k_dequantize<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(
+        (const long long*)n_theta, (const long long*)n_phi, theta, phi, n, make_params(layout));
+    return launch_status();
+}
+
+int vc3_encode_magnitude(const double* r, uint64_t* field, int64_t n, vc3_layout layout,
+                         void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    VC3_CHECK_N(n);
+    if (!r || !field) return VC3_ERR_ARG;
+    k_encode_mag<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(
+        r, (unsigned long long*)field, n, make_params(layout));
+    return launch_status();
+}
+
+int vc3_decode_magnitude(const int64_t* field, float* r, int64_t n, vc3_layout layout,
+                         void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    VC3_CHECK_N(n);
+    if (!r || !field) return VC3_ERR_ARG;
+    k_decode_mag<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>((const long long*)field, r, n,
+                                                                    make_params(layout));
+    return launch_status();
+}
+
+int vc3_magnitude_events(const float* xyz, int64_t n, vc3_layout layout,
+                         unsigned long long* d_counts, void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    VC3_CHECK_N(n);
+    if (!xyz || !d_counts) return VC3_ERR_ARG;
+    k_mag_events<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(xyz, n, make_params(layout),
+                                                                    d_counts);
+    return launch_status();
+}
+
+int vc3_error_stats(const float* v, const float* vh, int64_t n, int32_t normalised, int64_t chunk,
+                    double* d_chunk_stats, void* stream) {
+    VC3_CHECK_N(n);
+    if (!v || !vh || !d_chunk_stats || chunk <= 0) return VC3_ERR_ARG;
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    const int64_t slices64 = (std::min(chunk, n) + kStatSlice - 1) / kStatSlice;
+    if (slices64 > 65535 || nchunks > 65535) return VC3_ERR_ARG;
+    const int slices = (int)slices64;
+    cudaStream_t s = (cudaStream_t)stream;
+    Moments* part = nullptr;
+    int st = cuda_status(cudaMallocAsync((void**)&part, sizeof(Moments) * slices * nchunks, s));
+    if (st) return st;
+    k_err_partial<<<dim3(slices, (unsigned)nchunks), kStatThreads, 0, s>>>(v, vh, n, normalised,
+                                                                          chunk, slices, part);
+    k_err_final<<<grid_for(nchunks), kThreads, 0, s>>>(part, nchunks, slices, d_chunk_stats);
+    st = launch_status();
+    cudaFreeAsync(part, s);
+    return st;
+}
+
+}  // extern "C"
