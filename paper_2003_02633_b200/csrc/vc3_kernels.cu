@@ -4,15 +4,18 @@
 // Memory layout in HBM: compressed words are contiguous uint64
 // arrays moved as 16-byte ulonglong2 pairs; vectors are the caller's
 // array-of-structs float32 [n][3] moved as three 16-byte float4 per group of
-// four vectors.  Every kernel is a grid-stride streaming loop sized to a
-// multiple of the 148 SMs; nothing is staged through an uncompressed HBM
-// intermediate.
+// four vectors.  Every kernel is a grid-stride streaming loop over a grid
+// sized to a multiple of the SM count; nothing uncompressed touches HBM in
+// the fused operations.  Decoding kernels first copy the layout's sin/cos
+// table (<= 20.5 KB) from global memory into shared memory.
 #include <cuda_runtime.h>
 
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <map>
 #include <mutex>
+#include <vector>
 
 #include "../../include/vc3_b200.h"
 #include "vc3_device.cuh"
@@ -38,22 +41,30 @@ int cuda_status(cudaError_t e) {
 
 int launch_status() { return cuda_status(cudaGetLastError()); }
 
+int current_device() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev;
+}
+
 int sm_count() {
-    static int count = 0;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-            count = 148;
-    });
+    static std::mutex mu;
+    static std::map<int, int> counts;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = counts.find(dev);
+    if (it != counts.end()) return it->second;
+    int count = 0;
+    if (cudaDeviceGetAttribute(&count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || count <= 0)
+        count = 148;
+    counts[dev] = count;
     return count;
 }
 
 constexpr int kThreads = 256;
 
-// grid for `items` work items of one thread each: at most 8 resident CTAs per SM
-// worth of blocks (grid-stride beyond that), at least one.
+// grid for `items` work items of one thread each: at most `per_sm` CTAs per
+// SM (grid-stride beyond that), at least one.
 unsigned grid_for(int64_t items, int per_sm = 8) {
     int64_t blocks = (items + kThreads - 1) / kThreads;
     int64_t cap = (int64_t)sm_count() * per_sm;
@@ -72,10 +83,15 @@ bool layout_ok(const vc3_layout& L) {
     return true;
 }
 
+long long floor_div_pow2(long long a, int shift) {  // floor(a / 2^shift)
+    return a >= 0 ? (a >> shift) : -((-a + (1LL << shift) - 1) >> shift);
+}
+
 // Host derivation of the by-value parameter block.  The double expressions
-// are the reference's (_kernels.py:139-140) evaluated in IEEE double.
+// of the bucket arithmetic are the reference's (_kernels.py:139-140)
+// evaluated in IEEE double; the doubled forms are exact scalings of them.
 Params make_params(const vc3_layout& L) {
-    Params P;
+    Params P{};
     P.e = L.exponent_bits;
     P.m = L.mantissa_bits;
     P.p = L.phi_bits;
@@ -90,12 +106,107 @@ Params make_params(const vc3_layout& L) {
     P.nt_half = (double)P.ntmax / 2.0;
     P.t_scale = (double)P.ntmax / (2.0 * pi);
     P.p_scale = (double)P.npmax / pi;
-    P.t_step = pi / (2.0 * (double)P.ntmax);
-    P.p_step = pi / (2.0 * (double)P.npmax);
+    P.nt_half2 = 2.0 * P.nt_half;
+    P.t_scale2 = 2.0 * P.t_scale;
+    P.p_scale2 = 2.0 * P.p_scale;
     P.field_low = 2u << P.m;
     P.field_high = ((unsigned)(P.emax - 1) << P.m) | ((1u << P.m) - 1u);
+    // tools/exhaustive.cu: fused theta bucket == reference for every float32
+    // theta at widths 1..29 (t = 30 and 32 each have a handful of ties).
+    P.theta_fma = P.t <= 29;
+    // decode tables
+    P.table_mode = (P.t <= 20 && P.p <= 20) ? 1 : 0;
+    P.t_shift = P.t > 9 ? P.t - 9 : 0;
+    P.p_shift = P.p > 9 ? P.p - 9 : 0;
+    const long long half_t = P.t_shift ? (1LL << (P.t_shift - 1)) : 0;
+    const long long half_p = P.p_shift ? (1LL << (P.p_shift - 1)) : 0;
+    const long long lo_t = floor_div_pow2(-P.ntmax + half_t, P.t_shift);
+    const long long hi_t = floor_div_pow2(P.ntmax + half_t, P.t_shift);
+    P.t_off = (int)(-lo_t);
+    P.t_n = (int)(hi_t - lo_t + 1);
+    P.p_n = (int)(floor_div_pow2(P.npmax + half_p, P.p_shift) + 1);
+    P.p_base = P.t_n + 2;
+    P.tab_n = P.p_base + P.p_n + 1;
+    const long double pid = (long double)kPi;
+    P.t_delta = (double)(pid / (long double)P.ntmax);
+    P.p_delta = (double)(pid / (long double)P.npmax);
+    P.t_rcp = 1.0 / (double)P.ntmax;
+    P.p_rcp = 1.0 / (double)P.npmax;
     return P;
 }
+
+// sin/cos(RN(pi) * k / b) to double accuracy: exact quarter-turn reduction,
+// then long double libm.  Entries near a zero crossing keep full relative
+// accuracy because pi - RN(pi) enters separately.
+void sincos_host(long long k, long long b, double* s, double* c) {
+    const long double pid = (long double)kPi;
+    const long double tail = 1.2246467991473531772e-16L;  // pi - RN(pi)
+    const long long ak = k < 0 ? -k : k;
+    long long j = (4 * ak + b) / (2 * b);
+    if (k < 0) j = -j;
+    const long long m = 2 * k - j * b;
+    const long double psi = pid * (long double)m / (2.0L * (long double)b) - (long double)j * tail / 2.0L;
+    const long double sp = sinl(psi), cp = cosl(psi);
+    long double ss, cc;
+    switch (((j % 4) + 4) % 4) {
+        case 0: ss = sp; cc = cp; break;
+        case 1: ss = cp; cc = -sp; break;
+        case 2: ss = -sp; cc = -cp; break;
+        default: ss = -cp; cc = sp; break;
+    }
+    *s = (double)ss;
+    *c = (double)cc;
+}
+
+// Device-resident decode tables, built once per (device, t, p) and kept.
+struct TableKey {
+    int dev, t, p;
+    bool operator<(const TableKey& o) const {
+        return dev != o.dev ? dev < o.dev : (t != o.t ? t < o.t : p < o.p);
+    }
+};
+std::mutex g_tab_mu;
+std::map<TableKey, double2*> g_tabs;
+
+int get_table(const Params& P, const double2** out) {
+    *out = nullptr;
+    if (!P.table_mode) return VC3_OK;
+    const TableKey key{current_device(), P.t, P.p};
+    std::lock_guard<std::mutex> lock(g_tab_mu);
+    auto it = g_tabs.find(key);
+    if (it != g_tabs.end()) {
+        *out = it->second;
+        return VC3_OK;
+    }
+    // layout: [theta grid t_n][theta endpoints 2][phi grid p_n][phi pole 1]
+    std::vector<double2> h((size_t)P.tab_n);
+    for (int i = 0; i < P.t_n; ++i) {
+        double s, c;
+        sincos_host((long long)(i - P.t_off) << P.t_shift, P.ntmax, &s, &c);
+        h[i] = make_double2(s, c);
+    }
+    h[P.t_n] = make_double2(-kPiTail, -1.0);     // nt = 0:     sin(-RN(pi)), cos(-RN(pi))
+    h[P.t_n + 1] = make_double2(kPiTail, -1.0);  // nt = ntmax: sin(+RN(pi)), cos(+RN(pi))
+    for (int i = 0; i < P.p_n; ++i) {
+        double s, c;
+        sincos_host((long long)i << P.p_shift, P.npmax, &s, &c);
+        h[P.p_base + i] = make_double2(s, c);
+    }
+    h[P.p_base + P.p_n] = make_double2(0.0, -1.0);  // nph = npmax: the reference's exact pole
+    double2* d = nullptr;
+    int st = cuda_status(cudaMalloc((void**)&d, h.size() * sizeof(double2)));
+    if (st) return st;
+    st = cuda_status(cudaMemcpy(d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    if (st) {
+        cudaFree(d);
+        return st;
+    }
+    g_tabs[key] = d;
+    *out = d;
+    return VC3_OK;
+}
+
+size_t table_smem(const Params& P) { return P.table_mode ? (size_t)P.tab_n * sizeof(double2) : 0; }
 
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
@@ -129,49 +240,66 @@ __device__ __forceinline__ int64_t gtid() {
 }
 __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
 
+// Copy the decode table into shared memory (once per CTA; grids are capped
+// at a few CTAs per SM, so the copy is amortised over the whole stream).
+template <bool TABLE>
+__device__ __forceinline__ void load_table(double2* sm, const double2* __restrict__ g,
+                                           const Params& P) {
+    if (TABLE) {
+        const int n = P.tab_n;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = g[i];
+        __syncthreads();
+    }
+}
+
 // ===================== kernels ==============================================
 
 // K1 compress: 4 vectors (48 B in, 32 B out) per thread per step.
-template <unsigned POLICY, bool VEC>
+template <unsigned POLICY, bool NARROW>
 __global__ void __launch_bounds__(kThreads) k_compress(const float* __restrict__ xyz,
                                                        unsigned long long* __restrict__ out,
-                                                       int64_t n, Params P,
+                                                       int64_t n, Params P, bool vec,
                                                        int32_t* __restrict__ nonfinite) {
     int bad = 0;
-    const int64_t groups = VEC ? n / 4 : 0;
+    const int64_t groups = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
         const float* src = xyz + 12 * g;
         const float4 a = ld_stream_f4(src), b = ld_stream_f4(src + 4), c = ld_stream_f4(src + 8);
         bad += !finite3(a.x, a.y, a.z) + !finite3(a.w, b.x, b.y) + !finite3(b.z, b.w, c.x) +
                !finite3(c.y, c.z, c.w);
-        const unsigned long long w0 = compress_one<POLICY, kFma>(a.x, a.y, a.z, P);
-        const unsigned long long w1 = compress_one<POLICY, kFma>(a.w, b.x, b.y, P);
-        const unsigned long long w2 = compress_one<POLICY, kFma>(b.z, b.w, c.x, P);
-        const unsigned long long w3 = compress_one<POLICY, kFma>(c.y, c.z, c.w, P);
+        const unsigned long long w0 = compress_one<POLICY, kFma, NARROW>(a.x, a.y, a.z, P);
+        const unsigned long long w1 = compress_one<POLICY, kFma, NARROW>(a.w, b.x, b.y, P);
+        const unsigned long long w2 = compress_one<POLICY, kFma, NARROW>(b.z, b.w, c.x, P);
+        const unsigned long long w3 = compress_one<POLICY, kFma, NARROW>(c.y, c.z, c.w, P);
         st_u2(out + 4 * g, w0, w1);
         st_u2(out + 4 * g + 2, w2, w3);
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         const float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
         bad += !finite3(x, y, z);
-        out[i] = compress_one<POLICY, kFma>(x, y, z, P);
+        out[i] = compress_one<POLICY, kFma, NARROW>(x, y, z, P);
     }
     if (bad && nonfinite) atomicAdd(nonfinite, bad);
 }
 
 // K2 decompress: 4 words (32 B in, 48 B out) per thread per step.
-template <bool VEC>
+template <bool TABLE>
 __global__ void __launch_bounds__(kThreads) k_decompress(const unsigned long long* __restrict__ w,
                                                          float* __restrict__ xyz, int64_t n,
-                                                         Params P) {
-    const int64_t groups = VEC ? n / 4 : 0;
+                                                         Params P, bool vec,
+                                                         const double2* __restrict__ gtab) {
+    extern __shared__ double2 s_tab[];
+    load_table<TABLE>(s_tab, gtab, P);
+    const double2* tt = s_tab;
+    const double2* tp = s_tab + P.p_base;
+    const int64_t groups = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
         const ulonglong2 u = ld_stream_u2(w + 4 * g), v = ld_stream_u2(w + 4 * g + 2);
         float o[12];
-        decompress_one(u.x, P, o[0], o[1], o[2]);
-        decompress_one(u.y, P, o[3], o[4], o[5]);
-        decompress_one(v.x, P, o[6], o[7], o[8]);
-        decompress_one(v.y, P, o[9], o[10], o[11]);
+        decompress_one<TABLE>(u.x, P, tt, tp, o[0], o[1], o[2]);
+        decompress_one<TABLE>(u.y, P, tt, tp, o[3], o[4], o[5]);
+        decompress_one<TABLE>(v.x, P, tt, tp, o[6], o[7], o[8]);
+        decompress_one<TABLE>(v.y, P, tt, tp, o[9], o[10], o[11]);
         float* dst = xyz + 12 * g;
         st_f4(dst, o[0], o[1], o[2], o[3]);
         st_f4(dst + 4, o[4], o[5], o[6], o[7]);
@@ -179,7 +307,7 @@ __global__ void __launch_bounds__(kThreads) k_decompress(const unsigned long lon
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float x, y, z;
-        decompress_one(w[i], P, x, y, z);
+        decompress_one<TABLE>(w[i], P, tt, tp, x, y, z);
         xyz[3 * i] = x;
         xyz[3 * i + 1] = y;
         xyz[3 * i + 2] = z;
@@ -187,34 +315,41 @@ __global__ void __launch_bounds__(kThreads) k_decompress(const unsigned long lon
 }
 
 // K3 fused add: c = compress(decompress(a) + decompress(b)) (_kernels.py:348-359)
-template <unsigned POLICY>
+template <unsigned POLICY, bool TABLE>
 __device__ __forceinline__ unsigned long long add_one(unsigned long long a, unsigned long long b,
-                                                      const Params& P) {
+                                                      const Params& P, const double2* tt,
+                                                      const double2* tp) {
     float x1, y1, z1, x2, y2, z2;
-    decompress_one(a, P, x1, y1, z1);
-    decompress_one(b, P, x2, y2, z2);
-    return compress_one<POLICY, kFma>(__fadd_rn(x1, x2), __fadd_rn(y1, y2), __fadd_rn(z1, z2), P);
+    decompress_one<TABLE>(a, P, tt, tp, x1, y1, z1);
+    decompress_one<TABLE>(b, P, tt, tp, x2, y2, z2);
+    return compress_one<POLICY, kFma, TABLE>(__fadd_rn(x1, x2), __fadd_rn(y1, y2), __fadd_rn(z1, z2), P);
 }
 
-template <unsigned POLICY, bool VEC>
+template <unsigned POLICY, bool TABLE>
 __global__ void __launch_bounds__(kThreads) k_add(const unsigned long long* __restrict__ a,
                                                   const unsigned long long* __restrict__ b,
                                                   unsigned long long* __restrict__ c, int64_t n,
-                                                  Params P) {
-    const int64_t pairs = VEC ? n / 2 : 0;
+                                                  Params P, bool vec,
+                                                  const double2* __restrict__ gtab) {
+    extern __shared__ double2 s_tab[];
+    load_table<TABLE>(s_tab, gtab, P);
+    const double2* tt = s_tab;
+    const double2* tp = s_tab + P.p_base;
+    const int64_t pairs = vec ? n / 2 : 0;
     for (int64_t g = gtid(); g < pairs; g += gstride()) {
         const ulonglong2 u = ld_stream_u2(a + 2 * g), v = ld_stream_u2(b + 2 * g);
-        st_u2(c + 2 * g, add_one<POLICY>(u.x, v.x, P), add_one<POLICY>(u.y, v.y, P));
+        st_u2(c + 2 * g, add_one<POLICY, TABLE>(u.x, v.x, P, tt, tp),
+              add_one<POLICY, TABLE>(u.y, v.y, P, tt, tp));
     }
-    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride()) c[i] = add_one<POLICY>(a[i], b[i], P);
+    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride())
+        c[i] = add_one<POLICY, TABLE>(a[i], b[i], P, tt, tp);
 }
 
 // K5 uncompressed baseline: flat float32 add (_kernels.py:341-345)
-template <bool VEC>
 __global__ void __launch_bounds__(kThreads) k_add_raw(const float* __restrict__ a,
                                                       const float* __restrict__ b,
-                                                      float* __restrict__ c, int64_t n) {
-    const int64_t quads = VEC ? n / 4 : 0;
+                                                      float* __restrict__ c, int64_t n, bool vec) {
+    const int64_t quads = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < quads; g += gstride()) {
         const float4 u = ld_stream_f4(a + 4 * g), v = ld_stream_f4(b + 4 * g);
         st_f4(c + 4 * g, __fadd_rn(u.x, v.x), __fadd_rn(u.y, v.y), __fadd_rn(u.z, v.z),
@@ -224,68 +359,81 @@ __global__ void __launch_bounds__(kThreads) k_add_raw(const float* __restrict__ 
 }
 
 // K4 axpy: y' = compress(alpha*decode(x) + decode(y))
-template <unsigned POLICY>
+template <unsigned POLICY, bool TABLE>
 __device__ __forceinline__ unsigned long long axpy_one(float al, unsigned long long x,
-                                                       unsigned long long y, const Params& P) {
+                                                       unsigned long long y, const Params& P,
+                                                       const double2* tt, const double2* tp) {
     float x1, y1, z1, x2, y2, z2;
-    decompress_one(x, P, x1, y1, z1);
-    decompress_one(y, P, x2, y2, z2);
-    return compress_one<POLICY, kFma>(__fadd_rn(__fmul_rn(al, x1), x2),
+    decompress_one<TABLE>(x, P, tt, tp, x1, y1, z1);
+    decompress_one<TABLE>(y, P, tt, tp, x2, y2, z2);
+    return compress_one<POLICY, kFma, TABLE>(__fadd_rn(__fmul_rn(al, x1), x2),
                                       __fadd_rn(__fmul_rn(al, y1), y2),
                                       __fadd_rn(__fmul_rn(al, z1), z2), P);
 }
 
-template <unsigned POLICY, bool VEC>
+template <unsigned POLICY, bool TABLE>
 __global__ void __launch_bounds__(kThreads) k_axpy(float al, const unsigned long long* __restrict__ x,
                                                    const unsigned long long* y,
-                                                   unsigned long long* yo, int64_t n, Params P) {
-    const int64_t pairs = VEC ? n / 2 : 0;
+                                                   unsigned long long* yo, int64_t n, Params P,
+                                                   bool vec, const double2* __restrict__ gtab) {
+    extern __shared__ double2 s_tab[];
+    load_table<TABLE>(s_tab, gtab, P);
+    const double2* tt = s_tab;
+    const double2* tp = s_tab + P.p_base;
+    const int64_t pairs = vec ? n / 2 : 0;
     for (int64_t g = gtid(); g < pairs; g += gstride()) {
         const ulonglong2 u = ld_stream_u2(x + 2 * g);
         const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(y + 2 * g);  // may alias yo
-        st_u2(yo + 2 * g, axpy_one<POLICY>(al, u.x, v.x, P), axpy_one<POLICY>(al, u.y, v.y, P));
+        st_u2(yo + 2 * g, axpy_one<POLICY, TABLE>(al, u.x, v.x, P, tt, tp),
+              axpy_one<POLICY, TABLE>(al, u.y, v.y, P, tt, tp));
     }
-    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride()) yo[i] = axpy_one<POLICY>(al, x[i], y[i], P);
+    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride())
+        yo[i] = axpy_one<POLICY, TABLE>(al, x[i], y[i], P, tt, tp);
 }
 
 // K4b low-storage RK stage: dq' = a*dq + dt*R ; q' = q + b*dq'
-template <unsigned POLICY>
+template <unsigned POLICY, bool TABLE>
 __device__ __forceinline__ void rk_one(float ca, float cb, float dt, unsigned long long& q,
                                        unsigned long long& dq, unsigned long long r,
-                                       const Params& P) {
+                                       const Params& P, const double2* tt, const double2* tp) {
     float q0, q1, q2, d0, d1, d2, r0, r1, r2;
-    decompress_one(q, P, q0, q1, q2);
-    decompress_one(dq, P, d0, d1, d2);
-    decompress_one(r, P, r0, r1, r2);
+    decompress_one<TABLE>(q, P, tt, tp, q0, q1, q2);
+    decompress_one<TABLE>(dq, P, tt, tp, d0, d1, d2);
+    decompress_one<TABLE>(r, P, tt, tp, r0, r1, r2);
     d0 = __fadd_rn(__fmul_rn(ca, d0), __fmul_rn(dt, r0));
     d1 = __fadd_rn(__fmul_rn(ca, d1), __fmul_rn(dt, r1));
     d2 = __fadd_rn(__fmul_rn(ca, d2), __fmul_rn(dt, r2));
     q0 = __fadd_rn(q0, __fmul_rn(cb, d0));
     q1 = __fadd_rn(q1, __fmul_rn(cb, d1));
     q2 = __fadd_rn(q2, __fmul_rn(cb, d2));
-    dq = compress_one<POLICY, kFma>(d0, d1, d2, P);
-    q = compress_one<POLICY, kFma>(q0, q1, q2, P);
+    dq = compress_one<POLICY, kFma, TABLE>(d0, d1, d2, P);
+    q = compress_one<POLICY, kFma, TABLE>(q0, q1, q2, P);
 }
 
-template <unsigned POLICY, bool VEC>
+template <unsigned POLICY, bool TABLE>
 __global__ void __launch_bounds__(kThreads) k_rk(float ca, float cb, float dt,
                                                  unsigned long long* __restrict__ q,
                                                  unsigned long long* __restrict__ dq,
                                                  const unsigned long long* __restrict__ R,
-                                                 int64_t n, Params P) {
-    const int64_t pairs = VEC ? n / 2 : 0;
+                                                 int64_t n, Params P, bool vec,
+                                                 const double2* __restrict__ gtab) {
+    extern __shared__ double2 s_tab[];
+    load_table<TABLE>(s_tab, gtab, P);
+    const double2* tt = s_tab;
+    const double2* tp = s_tab + P.p_base;
+    const int64_t pairs = vec ? n / 2 : 0;
     for (int64_t g = gtid(); g < pairs; g += gstride()) {
         ulonglong2 u = *reinterpret_cast<const ulonglong2*>(q + 2 * g);
         ulonglong2 v = *reinterpret_cast<const ulonglong2*>(dq + 2 * g);
         const ulonglong2 r = ld_stream_u2(R + 2 * g);
-        rk_one<POLICY>(ca, cb, dt, u.x, v.x, r.x, P);
-        rk_one<POLICY>(ca, cb, dt, u.y, v.y, r.y, P);
+        rk_one<POLICY, TABLE>(ca, cb, dt, u.x, v.x, r.x, P, tt, tp);
+        rk_one<POLICY, TABLE>(ca, cb, dt, u.y, v.y, r.y, P, tt, tp);
         st_u2(q + 2 * g, u.x, u.y);
         st_u2(dq + 2 * g, v.x, v.y);
     }
     for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride()) {
         unsigned long long qq = q[i], dd = dq[i];
-        rk_one<POLICY>(ca, cb, dt, qq, dd, R[i], P);
+        rk_one<POLICY, TABLE>(ca, cb, dt, qq, dd, R[i], P, tt, tp);
         q[i] = qq;
         dq[i] = dd;
     }
@@ -475,11 +623,12 @@ int by_policy(uint32_t pol, A... args) {
 template <unsigned POL>
 struct RunCompress {
     static int run(const float* x, uint64_t* w, int64_t n, const Params& P, int32_t* nf, cudaStream_t s) {
-        if (aligned16(x) && aligned16(w)) {
-            k_compress<POL, true><<<grid_for((n + 3) / 4), kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, nf);
-        } else {
-            k_compress<POL, false><<<grid_for(n), kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, nf);
-        }
+        const bool vec = aligned16(x) && aligned16(w);
+        const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
+        if (P.t <= 29 && P.p <= 29)
+            k_compress<POL, true><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
+        else
+            k_compress<POL, false><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
         return launch_status();
     }
 };
@@ -487,13 +636,15 @@ struct RunCompress {
 template <unsigned POL>
 struct RunAdd {
     static int run(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t n, const Params& P,
-                   cudaStream_t s) {
+                   const double2* tab, cudaStream_t s) {
         auto A = (const unsigned long long*)a, B = (const unsigned long long*)b;
         auto C = (unsigned long long*)c;
-        if (aligned16(a) && aligned16(b) && aligned16(c))
-            k_add<POL, true><<<grid_for((n + 1) / 2), kThreads, 0, s>>>(A, B, C, n, P);
+        const bool vec = aligned16(a) && aligned16(b) && aligned16(c);
+        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
+        if (P.table_mode)
+            k_add<POL, true><<<grid, kThreads, table_smem(P), s>>>(A, B, C, n, P, vec, tab);
         else
-            k_add<POL, false><<<grid_for(n), kThreads, 0, s>>>(A, B, C, n, P);
+            k_add<POL, false><<<grid, kThreads, 0, s>>>(A, B, C, n, P, vec, tab);
         return launch_status();
     }
 };
@@ -501,13 +652,15 @@ struct RunAdd {
 template <unsigned POL>
 struct RunAxpy {
     static int run(float al, const uint64_t* x, const uint64_t* y, uint64_t* yo, int64_t n,
-                   const Params& P, cudaStream_t s) {
+                   const Params& P, const double2* tab, cudaStream_t s) {
         auto X = (const unsigned long long*)x, Y = (const unsigned long long*)y;
         auto O = (unsigned long long*)yo;
-        if (aligned16(x) && aligned16(y) && aligned16(yo))
-            k_axpy<POL, true><<<grid_for((n + 1) / 2), kThreads, 0, s>>>(al, X, Y, O, n, P);
+        const bool vec = aligned16(x) && aligned16(y) && aligned16(yo);
+        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
+        if (P.table_mode)
+            k_axpy<POL, true><<<grid, kThreads, table_smem(P), s>>>(al, X, Y, O, n, P, vec, tab);
         else
-            k_axpy<POL, false><<<grid_for(n), kThreads, 0, s>>>(al, X, Y, O, n, P);
+            k_axpy<POL, false><<<grid, kThreads, 0, s>>>(al, X, Y, O, n, P, vec, tab);
         return launch_status();
     }
 };
@@ -515,13 +668,15 @@ struct RunAxpy {
 template <unsigned POL>
 struct RunRk {
     static int run(float ca, float cb, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
-                   int64_t n, const Params& P, cudaStream_t s) {
+                   int64_t n, const Params& P, const double2* tab, cudaStream_t s) {
         auto Q = (unsigned long long*)q, D = (unsigned long long*)dq;
         auto RR = (const unsigned long long*)R;
-        if (aligned16(q) && aligned16(dq) && aligned16(R))
-            k_rk<POL, true><<<grid_for((n + 1) / 2), kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P);
+        const bool vec = aligned16(q) && aligned16(dq) && aligned16(R);
+        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
+        if (P.table_mode)
+            k_rk<POL, true><<<grid, kThreads, table_smem(P), s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
         else
-            k_rk<POL, false><<<grid_for(n), kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P);
+            k_rk<POL, false><<<grid, kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
         return launch_status();
     }
 };
@@ -544,7 +699,7 @@ struct RunSpherical {
 // ===================== extern "C" boundary ====================================
 extern "C" {
 
-const char* vc3_version(void) { return "vc3-b200 0.1.0 (sm_100a)"; }
+const char* vc3_version(void) { return "vc3-b200 0.2.0 (sm_100a)"; }
 
 const char* vc3_status_string(int status) {
     switch (status) {
@@ -577,11 +732,17 @@ int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layo
     VC3_CHECK_N(n);
     if (!xyz || !words) return VC3_ERR_ARG;
     const Params P = make_params(layout);
+    const double2* tab = nullptr;
+    int st = get_table(P, &tab);
+    if (st) return st;
     auto W = (const unsigned long long*)words;
-    if (aligned16(words) && aligned16(xyz))
-        k_decompress<true><<<grid_for((n + 3) / 4), kThreads, 0, (cudaStream_t)stream>>>(W, xyz, n, P);
+    const bool vec = aligned16(words) && aligned16(xyz);
+    const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (P.table_mode)
+        k_decompress<true><<<grid, kThreads, table_smem(P), s>>>(W, xyz, n, P, vec, tab);
     else
-        k_decompress<false><<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(W, xyz, n, P);
+        k_decompress<false><<<grid, kThreads, 0, s>>>(W, xyz, n, P, vec, tab);
     return launch_status();
 }
 
@@ -591,16 +752,19 @@ int vc3_add_compressed(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_
     if (policy > 7u) return VC3_ERR_ARG;
     VC3_CHECK_N(n);
     if (!a || !b || !c) return VC3_ERR_ARG;
-    return by_policy<RunAdd>(policy, a, b, c, n, make_params(layout), (cudaStream_t)stream);
+    const Params P = make_params(layout);
+    const double2* tab = nullptr;
+    int st = get_table(P, &tab);
+    if (st) return st;
+    return by_policy<RunAdd>(policy, a, b, c, n, P, tab, (cudaStream_t)stream);
 }
 
 int vc3_add_raw(const float* a, const float* b, float* c, int64_t n_floats, void* stream) {
     VC3_CHECK_N(n_floats);
     if (!a || !b || !c) return VC3_ERR_ARG;
-    if (aligned16(a) && aligned16(b) && aligned16(c))
-        k_add_raw<true><<<grid_for((n_floats + 3) / 4), kThreads, 0, (cudaStream_t)stream>>>(a, b, c, n_floats);
-    else
-        k_add_raw<false><<<grid_for(n_floats), kThreads, 0, (cudaStream_t)stream>>>(a, b, c, n_floats);
+    const bool vec = aligned16(a) && aligned16(b) && aligned16(c);
+    k_add_raw<<<grid_for(vec ? (n_floats + 3) / 4 : n_floats), kThreads, 0, (cudaStream_t)stream>>>(
+        a, b, c, n_floats, vec);
     return launch_status();
 }
 
@@ -610,8 +774,11 @@ int vc3_axpy(float alpha, const uint64_t* x, const uint64_t* y, uint64_t* y_out,
     if (policy > 7u) return VC3_ERR_ARG;
     VC3_CHECK_N(n);
     if (!x || !y || !y_out) return VC3_ERR_ARG;
-    return by_policy<RunAxpy>(policy, alpha, x, y, y_out, n, make_params(layout),
-                              (cudaStream_t)stream);
+    const Params P = make_params(layout);
+    const double2* tab = nullptr;
+    int st = get_table(P, &tab);
+    if (st) return st;
+    return by_policy<RunAxpy>(policy, alpha, x, y, y_out, n, P, tab, (cudaStream_t)stream);
 }
 
 int vc3_rk_stage(float a, float b, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
@@ -620,8 +787,11 @@ int vc3_rk_stage(float a, float b, float dt, uint64_t* q, uint64_t* dq, const ui
     if (policy > 7u) return VC3_ERR_ARG;
     VC3_CHECK_N(n);
     if (!q || !dq || !R) return VC3_ERR_ARG;
-    return by_policy<RunRk>(policy, a, b, dt, q, dq, R, n, make_params(layout),
-                            (cudaStream_t)stream);
+    const Params P = make_params(layout);
+    const double2* tab = nullptr;
+    int st = get_table(P, &tab);
+    if (st) return st;
+    return by_policy<RunRk>(policy, a, b, dt, q, dq, R, n, P, tab, (cudaStream_t)stream);
 }
 
 int vc3_to_spherical(const float* xyz, double* r, double* theta, double* phi, int64_t n,

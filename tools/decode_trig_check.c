@@ -101,6 +101,45 @@ static void hprint(const char* name, hist_t* H) {
            (long long)H->h[4], (long long)H->h[5], (long long)H->max, H->maxrel);
 }
 
+// Variant C: 1-level table + residual polynomial (the product decode).
+// Table entry for hi: (sin, cos)(RN(pi) * hi * 2^sh / b), evaluated in long double
+// after an exact quarter-turn reduction (so entries near zero crossings keep
+// full relative accuracy).  theta endpoints are special-cased by the caller.
+static void sincos_ld(int64_t k, int64_t b, double* s, double* c) {
+    // alpha = pi_d * k / b ; j = round(2k/b) ; residual = pi_d*(2k - j b)/(2b) - j*(pi - pi_d)/2
+    const long double PID = (long double)PI_;
+    const long double TAIL = 1.2246467991473531772e-16L;  // pi - RN(pi)
+    int64_t ak = k < 0 ? -k : k;
+    int64_t j = (4 * ak + b) / (2 * b);  // round(2|k|/b)
+    if (k < 0) j = -j;
+    int64_t m = 2 * k - j * b;
+    long double psi = PID * (long double)m / (2.0L * (long double)b) - (long double)j * TAIL / 2.0L;
+    long double sp = sinl(psi), cp = cosl(psi);
+    long double ss, cc;
+    switch (((j % 4) + 4) % 4) {
+        case 0: ss = sp; cc = cp; break;
+        case 1: ss = cp; cc = -sp; break;
+        case 2: ss = -sp; cc = -cp; break;
+        default: ss = -cp; cc = sp; break;
+    }
+    *s = (double)ss; *c = (double)cc;
+}
+
+static void sincos_tab1(int64_t a, int64_t b, int sh, double* s, double* c) {
+    const long double PID = (long double)PI_;
+    int64_t half = sh ? (1LL << (sh - 1)) : 0;
+    int64_t hi = (a + half) >> sh, lo = a - (hi << sh);
+    double sA, cA;
+    sincos_ld(hi << sh, b, &sA, &cA);
+    double delta = (double)(PID / (long double)b);
+    double psi = (double)lo * delta;
+    double u = psi * psi;
+    double sps = fma(psi * u, fma(u, 1.0 / 120.0, -1.0 / 6.0), psi);
+    double cm1 = u * fma(u, 1.0 / 24.0, -0.5);
+    *s = fma(cA, sps, fma(sA, cm1, sA));
+    *c = fma(-sA, sps, fma(cA, cm1, cA));
+}
+
 static uint64_t rng_state = 0x9E3779B97F4A7C15ull;
 static uint64_t rng(void) { rng_state ^= rng_state << 13; rng_state ^= rng_state >> 7; rng_state ^= rng_state << 17; return rng_state; }
 
@@ -112,8 +151,9 @@ static int e2e(void) {
     for (int64_t n = 0; n <= NP; ++n) { double ph = PI_ * (double)n / (double)NP; sp[n] = sin(ph); cp[n] = cos(ph); }
     sp[NP] = 0.0; cp[NP] = -1.0;
     double rN = 1.0 / (double)N, rNP = 1.0 / (double)NP;
-    int64_t total = 0, misA = 0, misB = 0, maxA = 0, maxB = 0;
+    int64_t total = 0, misA = 0, misB = 0, misC = 0;
     for (int64_t i = 0; i < 20000000; ++i) {
+        if ((i & 3) == 0) { /* force endpoints sometimes */ }
         uint64_t w = rng();
         int64_t nt = w & N, nph = (w >> t) & NP;
         uint32_t mant = (uint32_t)(w >> 40) & 0x7fffff;
@@ -129,6 +169,13 @@ static int e2e(void) {
         sincos_ref_angle(PI_ * (q - 1.0), j, &sB, &cB);
         if (nph == NP) { spB = 0; cpB = -1; }
         else { double qp = div_cr(PI_ * (double)nph, (double)NP, rNP); int jp = (4 * nph > NP) + (4 * nph > 3 * NP); sincos_ref_angle(qp, jp, &spB, &cpB); }
+        double sC, cC, spC, cpC;
+        sincos_tab1(2 * nt - N, N, 9, &sC, &cC);
+        if (nt == 0) { sC = -1.2246467991473532e-16; cC = -1.0; }
+        if (nt == N) { sC = 1.2246467991473532e-16; cC = -1.0; }
+        if (nph == NP) { spC = 0; cpC = -1; } else sincos_tab1(nph, NP, 9, &spC, &cpC);
+        float C[3] = {(float)(R * cC * spC), (float)(R * sC * spC), (float)(R * cpC)};
+        for (int k = 0; k < 3; ++k) misC += C[k] != ref[k];
         float A[3] = {(float)(R * cA * spA), (float)(R * sA * spA), (float)(R * cpA)};
         float B[3] = {(float)(R * cB * spB), (float)(R * sB * spB), (float)(R * cpB)};
         for (int k = 0; k < 3; ++k) {
@@ -139,6 +186,7 @@ static int e2e(void) {
             (void)dA; (void)dB;
         }
     }
+    printf("variant C (table) mismatches %lld\n", (long long)misC);
     printf("components %lld: variant A mismatches %lld (%.3g), variant B mismatches %lld (%.3g)\n",
            (long long)total, (long long)misA, (double)misA / total, (long long)misB, (double)misB / total);
     return 0;
@@ -146,8 +194,8 @@ static int e2e(void) {
 
 int main(int argc, char** argv) {
     if (argc > 1) return e2e();
-    int layouts[][2] = {{18, 17}, {16, 16}, {17, 16}, {17, 17}};
-    for (int li = 0; li < 4; ++li) {
+    int layouts[][2] = {{18, 17}, {16, 16}, {17, 16}, {17, 17}, {25, 10}, {8, 8}, {3, 2}};
+    for (int li = 0; li < 7; ++li) {
         int t = layouts[li][0], p = layouts[li][1];
         int64_t N = (1LL << t) - 1, NP = (1LL << p) - 1;
         printf("layout t=%d p=%d\n", t, p);
@@ -170,6 +218,23 @@ int main(int argc, char** argv) {
             hadd(&hsB, s, rs); hadd(&hcB, c, rc);
         }
         printf(" theta (%lld entries), div_cr mismatches %lld\n", (long long)(N + 1), (long long)divbad);
+        {
+            hist_t hs = {0}, hc = {0};
+            int shown = 0;
+            for (int64_t n = 0; n <= N; ++n) {
+                double th = PI_ * (2.0 * (double)n / (double)N - 1.0);
+                double rs = sin(th), rc = cos(th), s2, c2;
+                sincos_tab1(2 * n - N, N, t > 9 ? t - 9 : 0, &s2, &c2);
+                if (n == 0) { s2 = -1.2246467991473532e-16; c2 = -1.0; }
+                if (n == N) { s2 = 1.2246467991473532e-16; c2 = -1.0; }
+                hadd(&hs, s2, rs); hadd(&hc, c2, rc);
+                if ((ulpdiff(s2, rs) > 4 || ulpdiff(c2, rc) > 4) && shown < 6) {
+                    printf("    n=%lld a=%lld sin ref %.17g got %.17g (%lld ulp) cos ref %.17g got %.17g (%lld ulp)\n", (long long)n, (long long)(2*n-N), rs, s2, (long long)ulpdiff(s2, rs), rc, c2, (long long)ulpdiff(c2, rc));
+                    shown++;
+                }
+            }
+            hprint("C table1 sin", &hs); hprint("C table1 cos", &hc);
+        }
         hprint("A int-reduce sin", &hsA); hprint("A int-reduce cos", &hcA);
         hprint("B ref-angle sin", &hsB); hprint("B ref-angle cos", &hcB);
         hist_t psA = {0}, pcA = {0}, psB = {0}, pcB = {0};
@@ -186,6 +251,16 @@ int main(int argc, char** argv) {
             hadd(&psB, s, rs); hadd(&pcB, c, rc);
         }
         printf(" phi (%lld entries), div_cr mismatches %lld\n", (long long)NP, (long long)divbad_p);
+        {
+            hist_t hs = {0}, hc = {0};
+            for (int64_t n = 0; n < NP; ++n) {
+                double ph = PI_ * (double)n / (double)NP;
+                double s2, c2;
+                sincos_tab1(n, NP, p > 9 ? p - 9 : 0, &s2, &c2);
+                hadd(&hs, s2, sin(ph)); hadd(&hc, c2, cos(ph));
+            }
+            hprint("C table1 sin", &hs); hprint("C table1 cos", &hc);
+        }
         hprint("A int-reduce sin", &psA); hprint("A int-reduce cos", &pcA);
         hprint("B ref-angle sin", &psB); hprint("B ref-angle cos", &pcB);
     }
