@@ -124,6 +124,36 @@ int vc3_decode_magnitude(const int64_t* field, float* r, int64_t n, vc3_layout l
 int vc3_magnitude_events(const float* xyz, int64_t n, vc3_layout layout,
                          unsigned long long* d_counts, void* stream);
 
+/* ---- K7 variants (analysis.py:259-417) ------------------------------------
+ * Angle coding variants the reference evaluates in compand_study and
+ * split_sweep, as word formats (ours: the reference defines none):
+ *   compander: the layout's packing [magnitude | n_phi | n_theta] with
+ *              companded indices (Compander.encode/decode, analysis.py:342-393);
+ *   split:     [magnitude | J], J = n_phi*(n_theta_max+1) + n_theta in
+ *              total_bits = phi_bits + theta_bits (SplitConfig, joint_encode,
+ *              analysis.py:259-297).
+ * Angles use the reference's double pipeline (ORACLE policy); the decode
+ * uses double sin/cos and narrows to float32 like compand_study/split_sweep. */
+#define VC3_VARIANT_UNIFORM 0
+#define VC3_VARIANT_COSINE 1
+#define VC3_VARIANT_TANH 2
+#define VC3_VARIANT_SPLIT 3
+
+typedef struct vc3_variant {
+    int32_t kind;       /* VC3_VARIANT_* */
+    int32_t total_bits; /* split: joint index width (must equal phi_bits + theta_bits) */
+    int64_t n_phi_max;  /* split: n_phi_max (n_theta_max is derived, analysis.py:271-276) */
+    double gamma;       /* tanh compander strength (> 0) */
+} vc3_variant;
+
+int vc3_compress_variant(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout,
+                         vc3_variant variant, int32_t* d_nonfinite, void* stream);
+int vc3_decompress_variant(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout,
+                           vc3_variant variant, void* stream);
+/* bucket maxima the variant uses (split: derived n_theta_max) */
+int vc3_variant_maxima(vc3_layout layout, vc3_variant variant, int64_t* n_theta_max,
+                       int64_t* n_phi_max);
+
 /* ---- statistics (analysis.py:118-167) ------------------------------------ */
 
 /* Per-chunk error moments of e_i = ||v_i - vh_i||_2 (optionally / ||v_i||), in

@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libvc3_b200.so"
-SOURCES = ["vc3_kernels.cu", "vc3_host.cu"]
+SOURCES = ["vc3_kernels.cu", "vc3_host.cu", "vc3_variants.cu"]
 HEADERS = ["vc3_device.cuh"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

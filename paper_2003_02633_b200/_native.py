@@ -25,6 +25,15 @@ class Layout(ctypes.Structure):
         "exponent_bias")]
 
 
+class Variant(ctypes.Structure):
+    """``vc3_variant`` (include/vc3_b200.h)."""
+
+    _fields_ = [("kind", ctypes.c_int32), ("total_bits", ctypes.c_int32),
+                ("n_phi_max", ctypes.c_int64), ("gamma", ctypes.c_double)]
+
+
+VARIANT_UNIFORM, VARIANT_COSINE, VARIANT_TANH, VARIANT_SPLIT = 0, 1, 2, 3
+
 _p = ctypes.c_void_p
 _i64 = ctypes.c_int64
 _i32 = ctypes.c_int32
@@ -50,6 +59,9 @@ SIGNATURES = {
     "vc3_decode_magnitude": ([_p, _p, _i64, Layout, _p], ctypes.c_int),
     "vc3_magnitude_events": ([_p, _i64, Layout, _p, _p], ctypes.c_int),
     "vc3_error_stats": ([_p, _p, _i64, _i32, _i64, _p, _p], ctypes.c_int),
+    "vc3_compress_variant": ([_p, _p, _i64, Layout, Variant, _p, _p], ctypes.c_int),
+    "vc3_decompress_variant": ([_p, _p, _i64, Layout, Variant, _p], ctypes.c_int),
+    "vc3_variant_maxima": ([Layout, Variant, _p, _p], ctypes.c_int),
     "vc3_add_compressed_host": ([_p, _p, _p, _i64, Layout, _u32, _i32], ctypes.c_int),
     "vc3_compress_host": ([_p, _p, _i64, Layout, _u32, _p, _i32], ctypes.c_int),
     "vc3_decompress_host": ([_p, _p, _i64, Layout, _i32], ctypes.c_int),

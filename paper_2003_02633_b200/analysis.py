@@ -202,3 +202,18 @@ def error_study_sharded(domain: SampleDomain, layout=DEFAULT_LAYOUT, policy=DEFA
     for row in table:
         acc.add(int(row[0]), float(row[1]), float(row[2]), float(row[3]))
     return acc.stats(normalised)
+
+
+# K7 variants (analysis.py:259-417) live in variants.py; re-exported here so
+# ``analysis.Compander`` etc. resolve as in the reference.
+from .variants import (  # noqa: E402,F401
+    Compander,
+    SplitConfig,
+    _quantize_free,
+    compand,
+    compand_inverse,
+    compand_study,
+    joint_decode,
+    joint_encode,
+    split_sweep,
+)

@@ -198,6 +198,42 @@ def main():
             d[f"err_sphere_{pname}_{int(norm)}"] = np.array(
                 [st.mean, st.max, st.stddev, st.count], dtype=np.float64)
 
+    # K7 variants (analysis.py:259-417): per-vector indices and reconstructions
+    # exactly as compand_study / split_sweep compute them, plus the studies.
+    vv = np.concatenate([sphere, mixed[:2000]])
+    d["var_vec"] = vv
+    r, th, ph = vc3.to_spherical(vv, ORACLE_POLICY)
+    rh = vc3.decode_magnitude(vc3.encode_magnitude(r, DEFAULT_LAYOUT), DEFAULT_LAYOUT).astype(np.float64)
+    ntmax, npmax = DEFAULT_LAYOUT.n_theta_max, DEFAULT_LAYOUT.n_phi_max
+    comps = {"uniform": analysis.Compander("uniform"), "cosine": analysis.Compander("cosine"),
+             "tanh05": analysis.Compander("tanh", 0.5), "tanh2": analysis.Compander("tanh", 2.0)}
+    for cname, comp in comps.items():
+        nt = comp.encode((th + np.pi) / (2.0 * np.pi), ntmax)
+        nph = comp.encode(ph / np.pi, npmax)
+        th2 = 2.0 * np.pi * comp.decode(nt, ntmax) - np.pi
+        ph2 = np.pi * comp.decode(nph, npmax)
+        sp = np.sin(ph2)
+        vh = np.stack([rh * np.cos(th2) * sp, rh * np.sin(th2) * sp, rh * np.cos(ph2)],
+                      axis=1).astype(np.float32)
+        d[f"cmp_{cname}_nt"], d[f"cmp_{cname}_nph"], d[f"cmp_{cname}_vh"] = nt, nph, vh
+        st = analysis.compand_study(analysis.SampleDomain("unit_sphere", 100_000, 11), comp)
+        d[f"cmp_{cname}_study"] = np.array([st.mean, st.max, st.stddev, st.count])
+    splits = [1 << 16, 98304, 1 << 17, 196608, 1 << 18]
+    d["split_values"] = np.array(splits)
+    for s_ in splits:
+        cfg = analysis.SplitConfig(35, s_ - 1)
+        nt, nph = analysis._quantize_free(th, ph, cfg.n_theta_max, cfg.n_phi_max)
+        J = analysis.joint_encode(nt, nph, cfg)
+        nt2, nph2 = analysis.joint_decode(J, cfg)
+        th2 = np.pi * (2.0 * nt2 / cfg.n_theta_max - 1.0)
+        ph2 = np.pi * nph2 / cfg.n_phi_max
+        sp = np.sin(ph2)
+        vh = np.stack([rh * np.cos(th2) * sp, rh * np.sin(th2) * sp, rh * np.cos(ph2)],
+                      axis=1).astype(np.float32)
+        d[f"split_{s_}_J"], d[f"split_{s_}_vh"] = J, vh
+    rows = analysis.split_sweep(35, splits, analysis.SampleDomain("unit_sphere", 100_000, 7))
+    d["split_study"] = np.array([[st.mean, st.max, st.stddev, st.count] for _, st in rows])
+
     np.savez_compressed(OUT / "golden.npz", **d)
     total = sum(v.nbytes for v in d.values())
     print(f"wrote {len(d)} arrays ({total / 1e6:.1f} MB raw) to {OUT / 'golden.npz'}")

@@ -1,0 +1,139 @@
+"""K7 variants on the GPU vs the reference (golden) and the numpy oracle.
+
+Angles run the reference's double pipeline; CUDA's libm may differ from
+glibc's by an ulp, so a bucket can flip at a tie (counted, each within one
+bin); reconstructions must be within 2 ulp and almost always exact."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import layout_by_name
+from test_gpu_parity import ulp32
+
+pytestmark = pytest.mark.gpu
+
+
+def assert_vectors_match(got, want, label):
+    """Variant reconstructions go through double libm transcendentals
+    (cos/acos/tanh/atanh) whose last-ulp differences between CUDA and glibc
+    are amplified in components that are ~1e-16 of the vector (angles at
+    +-pi): compare components to 2 ulp or 1e-13 of the vector norm."""
+    got = np.asarray(got, np.float32)
+    want = np.asarray(want, np.float32)
+    u = ulp32(got, want)
+    norm = np.linalg.norm(want.astype(np.float64), axis=1, keepdims=True)
+    absdiff = np.abs(got.astype(np.float64) - want.astype(np.float64))
+    assert ((u <= 2) | (absdiff <= 1e-13 * norm)).all(), f"{label}: max ulp {u.max()}"
+    assert (u == 0).mean() >= 0.999, f"{label}: exact fraction {(u == 0).mean()}"
+
+COMPANDERS = {"uniform": ("uniform", 0.5), "cosine": ("cosine", 0.5),
+              "tanh05": ("tanh", 0.5), "tanh2": ("tanh", 2.0)}
+
+
+def _tie_check(got, want, label, keep=None):
+    """Bucket ties within one bin.  ``keep`` masks out zero vectors: the word
+    format stores them as the all-zero word (their angles carry no data)."""
+    got, want = np.asarray(got, np.int64), np.asarray(want, np.int64)
+    if keep is not None:
+        got, want = got[keep], want[keep]
+    diff = got != want
+    assert (np.abs(got - want) <= 1).all(), label
+    assert diff.mean() <= 1e-3, f"{label}: tie rate {diff.mean():.2e}"
+    return int(diff.sum())
+
+
+@pytest.mark.parametrize("cname", list(COMPANDERS))
+def test_compander_round_trip_golden(golden, vc3b, cuda, cname):
+    from paper_2003_02633_b200 import variants
+
+    lay = layout_by_name("17_18")
+    comp = variants.Compander(*COMPANDERS[cname])
+    v = golden["var_vec"]
+    words = variants.compress_variant(v, comp, lay)
+    nt = (words & np.uint64(lay.n_theta_max)).astype(np.int64)
+    nph = ((words >> np.uint64(18)) & np.uint64(lay.n_phi_max)).astype(np.int64)
+    keep = np.linalg.norm(v, axis=1) > 0
+    ties = _tie_check(nt, golden[f"cmp_{cname}_nt"], f"{cname} theta", keep)
+    ties += _tie_check(nph, golden[f"cmp_{cname}_nph"], f"{cname} phi", keep)
+    print(f"{cname}: {ties} bucket ties")
+    vh = variants.decompress_variant(words, comp, lay)
+    same = (nt == golden[f"cmp_{cname}_nt"]) & (nph == golden[f"cmp_{cname}_nph"])
+    same &= np.linalg.norm(v, axis=1) > 0
+    assert_vectors_match(vh[same], golden[f"cmp_{cname}_vh"][same], cname)
+
+
+def test_split_round_trip_golden(golden, vc3b, cuda):
+    from paper_2003_02633_b200 import variants
+
+    lay = layout_by_name("17_18")
+    v = golden["var_vec"]
+    for s in golden["split_values"]:
+        cfg = variants.SplitConfig(35, int(s) - 1)
+        assert variants.variant_maxima(cfg, lay) == (cfg.n_theta_max, cfg.n_phi_max)
+        words = variants.compress_variant(v, cfg, lay)
+        J = (words & np.uint64((1 << 35) - 1)).astype(np.int64)
+        want = golden[f"split_{s}_J"]
+        gt, gp = variants.joint_decode(J, cfg)
+        wt, wp = variants.joint_decode(want, cfg)
+        keep = np.linalg.norm(v, axis=1) > 0
+        _tie_check(gt, wt, f"split {s} theta", keep)
+        _tie_check(gp, wp, f"split {s} phi", keep)
+        vh = variants.decompress_variant(words, cfg, lay)
+        same = (J == want) & (np.linalg.norm(v, axis=1) > 0)
+        assert_vectors_match(vh[same], golden[f"split_{s}_vh"][same], f"split {s}")
+
+
+def test_variant_studies_match_reference(golden, vc3b, cuda):
+    from paper_2003_02633_b200 import analysis
+
+    for cname, (kind, gamma) in COMPANDERS.items():
+        st = analysis.compand_study(analysis.SampleDomain("unit_sphere", 100_000, 11),
+                                    analysis.Compander(kind, gamma))
+        ref = golden[f"cmp_{cname}_study"]
+        assert st.count == int(ref[3])
+        assert st.mean == pytest.approx(ref[0], rel=1e-9)
+        assert st.stddev == pytest.approx(ref[2], rel=1e-6)
+        assert st.max == pytest.approx(ref[1], rel=1e-6)
+    rows = analysis.split_sweep(35, golden["split_values"].tolist(),
+                                analysis.SampleDomain("unit_sphere", 100_000, 7))
+    for (cfg, st), ref in zip(rows, golden["split_study"]):
+        assert st.mean == pytest.approx(ref[0], rel=1e-9)
+        assert st.max == pytest.approx(ref[1], rel=1e-6)
+
+
+def test_error_study_matches_reference(golden, vc3b, cuda):
+    from paper_2003_02633_b200 import analysis
+
+    for code, pol in (("SDS", vc3b.DEFAULT_POLICY), ("DDD", vc3b.ORACLE_POLICY)):
+        for norm in (False, True):
+            st = analysis.error_study(analysis.SampleDomain("unit_sphere", 60_000, 21),
+                                      vc3b.DEFAULT_LAYOUT, pol, normalised=norm)
+            ref = golden[f"err_sphere_{code}_{int(norm)}"]
+            assert st.count == int(ref[3])
+            assert st.mean == pytest.approx(ref[0], rel=1e-9)
+            assert st.stddev == pytest.approx(ref[2], rel=1e-6)
+            assert st.max == pytest.approx(ref[1], rel=1e-6)
+
+
+def test_variants_larger_vs_oracle(vc3b, oracle, cuda):
+    import vc3_variants
+
+    from paper_2003_02633_b200 import variants
+
+    lay = layout_by_name("17_18")
+    g = np.random.Generator(np.random.Philox(31))
+    v = (g.normal(size=(1 << 18, 3)) * 10.0 ** g.uniform(-3, 3, (1 << 18, 1))).astype(np.float32)
+    dv = torch.from_numpy(v).to(cuda)
+    comp = variants.Compander("tanh", 0.5)
+    nt, nph, vh = vc3_variants.compand_round_trip(v, lay, "tanh", 0.5)
+    w = variants.compress_variant(dv, comp, lay).cpu().numpy()
+    _tie_check((w & np.uint64(lay.n_theta_max)).astype(np.int64), nt, "tanh theta",
+               np.linalg.norm(v, axis=1) > 0)
+    cfg = variants.SplitConfig(35, 98303)
+    J, vh2 = vc3_variants.split_round_trip(v, lay, 35, 98303)
+    w2 = variants.compress_variant(dv, cfg, lay).cpu().numpy()
+    same = (w2 & np.uint64((1 << 35) - 1)).astype(np.int64) == J
+    assert same.mean() > 0.999
+    out = variants.decompress_variant(torch.from_numpy(w2).to(cuda), cfg, lay).cpu().numpy()
+    assert_vectors_match(out[same], vh2[same], "split 98304")

@@ -141,3 +141,29 @@ def test_threaded_equals_serial(golden, oracle):
                           oracle.add_compressed(a, b, lay, pol, nthreads=1))
     v = golden["vec_mixed"]
     assert np.array_equal(oracle.compress(v, lay, pol, nthreads=3), oracle.compress(v, lay, pol))
+
+
+COMPANDERS = {"uniform": ("uniform", 0.5), "cosine": ("cosine", 0.5),
+              "tanh05": ("tanh", 0.5), "tanh2": ("tanh", 2.0)}
+
+
+@pytest.mark.parametrize("cname", list(COMPANDERS))
+def test_variant_oracle_compand(golden, oracle, cname):
+    import vc3_variants
+
+    kind, gamma = COMPANDERS[cname]
+    nt, nph, vh = vc3_variants.compand_round_trip(golden["var_vec"], layout_by_name("17_18"),
+                                                  kind, gamma)
+    assert np.array_equal(nt, golden[f"cmp_{cname}_nt"])
+    assert np.array_equal(nph, golden[f"cmp_{cname}_nph"])
+    assert np.array_equal(vh.view(np.uint32), golden[f"cmp_{cname}_vh"].view(np.uint32))
+
+
+def test_variant_oracle_split(golden, oracle):
+    import vc3_variants
+
+    for s in golden["split_values"]:
+        J, vh = vc3_variants.split_round_trip(golden["var_vec"], layout_by_name("17_18"), 35,
+                                              int(s) - 1)
+        assert np.array_equal(J, golden[f"split_{s}_J"])
+        assert np.array_equal(vh.view(np.uint32), golden[f"split_{s}_vh"].view(np.uint32))
