@@ -228,6 +228,87 @@ def time_region(fn, steps, stream, torch):
     return start.elapsed_time(end) / steps  # ms
 
 
+def run_secondary(args, vc3b, lib, dev, stream, n):
+    """BASELINE configs C3 (variant codecs) and C4 (RK stage on an ICV field),
+    each timed with CUDA events on the launching stream."""
+    import torch
+
+    from paper_2003_02633_b200 import _native, fields, variants
+
+    lay = vc3b.DEFAULT_LAYOUT
+    cl = _native.c_layout(lay)
+    out = {}
+    steps = max(3, min(args.steps, 10))
+
+    # C3: companding + fractional splitting, round trip on n cube vectors
+    gen = torch.Generator(device=dev).manual_seed(99)
+    v = torch.rand((n, 3), device=dev, generator=gen).mul_(2).sub_(1)
+    w = torch.empty(n, dtype=torch.uint64, device=dev)
+    vh = torch.empty_like(v)
+    c3 = {}
+    for name, var in (("uniform", variants.Compander("uniform")),
+                      ("cosine", variants.Compander("cosine")),
+                      ("tanh_0.5", variants.Compander("tanh", 0.5)),
+                      ("tanh_2.0", variants.Compander("tanh", 2.0)),
+                      ("split_98304", variants.SplitConfig(35, 98303))):
+        cv = variants.c_variant(var, lay)
+        enc = lambda: lib.vc3_compress_variant(v.data_ptr(), w.data_ptr(), n, cl, cv, None,
+                                              stream.cuda_stream)
+        dec = lambda: lib.vc3_decompress_variant(w.data_ptr(), vh.data_ptr(), n, cl, cv,
+                                                stream.cuda_stream)
+        enc(); dec()
+        torch.cuda.synchronize()
+        te = time_region(enc, steps, stream, torch)
+        td = time_region(dec, steps, stream, torch)
+        c3[name] = {"compress_gvec_s": n / (te * 1e-3) / 1e9,
+                    "decompress_gvec_s": n / (td * 1e-3) / 1e9}
+    out["C3_variants"] = {"n_vectors": n, "unit": UNIT, "results": c3,
+                          "note": "double-precision ORACLE-policy angles + CUDA libm "
+                                  "transcendentals, as the reference's studies"}
+    del v, w, vh
+
+    # C4: low-storage RK stage on compressed momentum of an isentropic vortex
+    n_elem = n // 125
+    mom, vel = fields.icv_fields(n_elem, 30.0, device=dev)
+    npts = mom.shape[0]
+    pol = vc3b.ALL_SINGLE_POLICY
+    q = vc3b.compress(mom, lay, pol)
+    dq = vc3b.compress(vel * 1e-3, lay, pol)
+    R = vc3b.compress(vel, lay, pol)
+    qf, dqf, Rf = mom.reshape(-1).clone(), (vel * 1e-3).reshape(-1), vel.reshape(-1)
+    del mom
+    k = [0]
+
+    def rk():
+        s_ = k[0] % 5
+        k[0] += 1
+        lib.vc3_rk_stage(float(fields.LSRK_A[s_]), float(fields.LSRK_B[s_]), 1e-3, q.data_ptr(),
+                         dq.data_ptr(), R.data_ptr(), npts, cl, pol.mask, stream.cuda_stream)
+
+    def rk32():
+        s_ = k[0] % 5
+        k[0] += 1
+        lib.vc3_rk_stage_f32(float(fields.LSRK_A[s_]), float(fields.LSRK_B[s_]), 1e-3,
+                             qf.data_ptr(), dqf.data_ptr(), Rf.data_ptr(), 3 * npts,
+                             stream.cuda_stream)
+
+    rk(); rk32()
+    torch.cuda.synchronize()
+    tc = time_region(rk, steps, stream, torch)
+    tf = time_region(rk32, steps, stream, torch)
+    out["C4_rk_stage_icv"] = {
+        "n_points": npts, "field": "ICV beta=5 gamma=1.4 psi=30deg, k=4 FR points, "
+                                   "[n_upts][n_elem] rows", "unit": UNIT,
+        "compressed_gvec_s": npts / (tc * 1e-3) / 1e9,
+        "compressed_hbm_gb_s": 40 * npts / (tc * 1e-3) / 1e9,
+        "fp32_gvec_s": npts / (tf * 1e-3) / 1e9,
+        "fp32_hbm_gb_s": 60 * npts / (tf * 1e-3) / 1e9,
+        "speedup_vs_fp32": tf / tc}
+    del q, dq, R, qf, dqf, Rf, vel
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_gpu(args, world, rank, local):
     import torch
 
@@ -353,6 +434,8 @@ def run_gpu(args, world, rank, local):
     if not np.array_equal(hc, c.cpu().numpy()):
         raise RuntimeError("host-API result differs from the device kernel result")
 
+    secondary_configs = {} if args.no_secondary else run_secondary(args, vc3b, lib, dev, stream, n)
+
     peak, peak_src = measured_peak()
     achieved = BYTES_COMPRESSED * n / (ms * 1e-3) / 1e9
     traffic = ncu_traffic()
@@ -374,6 +457,7 @@ def run_gpu(args, world, rank, local):
                      "kernel": "k_add<7,true> (fused decompress-add-recompress)",
                      "algorithmic_bytes_per_launch": BYTES_COMPRESSED * n},
         "secondary_kernels": sec,
+        "secondary_configs": secondary_configs,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 16 * e2e_n,
                 "d2h_bytes_per_step": 8 * e2e_n,
                 "path": "vc3_add_compressed_host (C ABI; paper_2003_02633_b200.add_compressed "
@@ -396,6 +480,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="vectors per GPU")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the C3/C4 secondary configs (quick runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)

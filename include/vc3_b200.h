@@ -101,6 +101,11 @@ int vc3_axpy(float alpha, const uint64_t* x, const uint64_t* y, uint64_t* y_out,
 int vc3_rk_stage(float a, float b, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
                  int64_t n, vc3_layout layout, uint32_t policy, void* stream);
 
+/* Uncompressed float32 baseline of vc3_rk_stage (60 B of HBM traffic per
+ * vector): the same op order on flat float32 arrays of n_floats elements. */
+int vc3_rk_stage_f32(float a, float b, float dt, float* q, float* dq, const float* R,
+                     int64_t n_floats, void* stream);
+
 /* ---- pieces (codec.py:99-186) -------------------------------------------- */
 
 /* codec.to_spherical (codec.py:99-114) -> spherical_kernel (_kernels.py:223-229) */

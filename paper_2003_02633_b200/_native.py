@@ -52,6 +52,7 @@ SIGNATURES = {
     "vc3_add_raw": ([_p, _p, _p, _i64, _p], ctypes.c_int),
     "vc3_axpy": ([_f32, _p, _p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
     "vc3_rk_stage": ([_f32, _f32, _f32, _p, _p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
+    "vc3_rk_stage_f32": ([_f32, _f32, _f32, _p, _p, _p, _i64, _p], ctypes.c_int),
     "vc3_to_spherical": ([_p, _p, _p, _p, _i64, _u32, _p, _p], ctypes.c_int),
     "vc3_quantize_angles": ([_p, _p, _p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
     "vc3_dequantize_angles": ([_p, _p, _p, _p, _i64, Layout, _p], ctypes.c_int),

@@ -358,6 +358,34 @@ __global__ void __launch_bounds__(kThreads) k_add_raw(const float* __restrict__ 
     for (int64_t i = quads * 4 + gtid(); i < n; i += gstride()) c[i] = __fadd_rn(a[i], b[i]);
 }
 
+// K5b uncompressed RK-stage baseline: dq' = a*dq + dt*R ; q' = q + b*dq' (flat float32)
+__global__ void __launch_bounds__(kThreads) k_rk_f32(float ca, float cb, float dt,
+                                                     float* __restrict__ q, float* __restrict__ dq,
+                                                     const float* __restrict__ R, int64_t n,
+                                                     bool vec) {
+    const int64_t quads = vec ? n / 4 : 0;
+    for (int64_t g = gtid(); g < quads; g += gstride()) {
+        float4 qv = *reinterpret_cast<const float4*>(q + 4 * g);
+        float4 dv = *reinterpret_cast<const float4*>(dq + 4 * g);
+        const float4 rv = ld_stream_f4(R + 4 * g);
+        dv.x = __fadd_rn(__fmul_rn(ca, dv.x), __fmul_rn(dt, rv.x));
+        dv.y = __fadd_rn(__fmul_rn(ca, dv.y), __fmul_rn(dt, rv.y));
+        dv.z = __fadd_rn(__fmul_rn(ca, dv.z), __fmul_rn(dt, rv.z));
+        dv.w = __fadd_rn(__fmul_rn(ca, dv.w), __fmul_rn(dt, rv.w));
+        qv.x = __fadd_rn(qv.x, __fmul_rn(cb, dv.x));
+        qv.y = __fadd_rn(qv.y, __fmul_rn(cb, dv.y));
+        qv.z = __fadd_rn(qv.z, __fmul_rn(cb, dv.z));
+        qv.w = __fadd_rn(qv.w, __fmul_rn(cb, dv.w));
+        st_f4(dq + 4 * g, dv.x, dv.y, dv.z, dv.w);
+        st_f4(q + 4 * g, qv.x, qv.y, qv.z, qv.w);
+    }
+    for (int64_t i = quads * 4 + gtid(); i < n; i += gstride()) {
+        const float d = __fadd_rn(__fmul_rn(ca, dq[i]), __fmul_rn(dt, R[i]));
+        dq[i] = d;
+        q[i] = __fadd_rn(q[i], __fmul_rn(cb, d));
+    }
+}
+
 // K4 axpy: y' = compress(alpha*decode(x) + decode(y))
 template <unsigned POLICY, bool TABLE>
 __device__ __forceinline__ unsigned long long axpy_one(float al, unsigned long long x,
@@ -792,6 +820,16 @@ int vc3_rk_stage(float a, float b, float dt, uint64_t* q, uint64_t* dq, const ui
     int st = get_table(P, &tab);
     if (st) return st;
     return by_policy<RunRk>(policy, a, b, dt, q, dq, R, n, P, tab, (cudaStream_t)stream);
+}
+
+int vc3_rk_stage_f32(float a, float b, float dt, float* q, float* dq, const float* R,
+                     int64_t n_floats, void* stream) {
+    VC3_CHECK_N(n_floats);
+    if (!q || !dq || !R) return VC3_ERR_ARG;
+    const bool vec = aligned16(q) && aligned16(dq) && aligned16(R);
+    k_rk_f32<<<grid_for(vec ? (n_floats + 3) / 4 : n_floats), kThreads, 0, (cudaStream_t)stream>>>(
+        a, b, dt, q, dq, R, n_floats, vec);
+    return launch_status();
 }
 
 int vc3_to_spherical(const float* xyz, double* r, double* theta, double* phi, int64_t n,

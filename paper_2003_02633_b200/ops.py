@@ -120,3 +120,19 @@ def rk_stage(a, b, dt, q, dq, R, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY
         q[...] = _dev.download(tq)
         dq[...] = _dev.download(tdq)
     return q, dq
+
+
+def rk_stage_f32(a, b, dt, q, dq, R):
+    """Uncompressed float32 RK stage on CUDA tensors (the baseline of
+    ``rk_stage``): dq <- a*dq + dt*R ; q <- q + b*dq, in place."""
+    lib = _native.load()
+    if not (_dev.is_device(q) and q.is_contiguous() and dq.is_contiguous()):
+        raise ValueError("rk_stage_f32 takes contiguous CUDA float32 tensors")
+    if not (q.numel() == dq.numel() == R.numel()):
+        raise LengthMismatch("q, dq and R must have the same length")
+    Rc = R.contiguous()
+    _native.check(lib.vc3_rk_stage_f32(float(np.float32(a)), float(np.float32(b)),
+                                       float(np.float32(dt)), q.data_ptr(), dq.data_ptr(),
+                                       Rc.data_ptr(), q.numel(), _dev.stream_of(q)),
+                  "rk_stage_f32")
+    return q, dq

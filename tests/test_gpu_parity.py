@@ -362,3 +362,39 @@ def test_full_size_fused_equals_composed_and_commutes(vc3b, cuda):
     w2 = vc3b.compress(v1, lay, vc3b.ORACLE_POLICY)
     assert torch.equal(w1.view(torch.int64), w2.view(torch.int64))
     assert torch.isfinite(vc3b.decompress(c.view(torch.int64)[idx], lay)).all()
+
+
+def test_rk_stage_on_icv_field_vs_composition(vc3b, oracle, cuda):
+    """BASELINE config C4 at the paper's mesh size (10^5 points):
+    five low-storage RK stages on compressed momentum match the oracle
+    composition (decompress, float32 update, compress) stage by stage."""
+    from paper_2003_02633_b200 import fields
+
+    lay, pol = layout_by_name("17_18"), policy_by_code("SSS")
+    mom, vel = fields.icv_fields(800, 30.0)
+    assert mom.shape == (100_000, 3) and (mom[:, 2] == 0).all()
+    q = oracle.compress(mom, lay, pol)
+    assert (((q >> np.uint64(18)) & np.uint64(lay.n_phi_max)) == 65536).all()  # equator
+    dq = oracle.compress(vel * np.float32(1e-3), lay, pol)
+    R = oracle.compress(vel, lay, pol)
+    tq, tdq, tR = (torch.from_numpy(x.copy()).to(cuda) for x in (q, dq, R))
+    dt = np.float32(1e-3)
+    for s in range(5):
+        a, b = np.float32(fields.LSRK_A[s]), np.float32(fields.LSRK_B[s])
+        vc3b.rk_stage(a, b, dt, tq, tdq, tR, lay, pol)
+        qd, dqd, Rd = (oracle.decompress(x, lay) for x in (q, dq, R))
+        dq_new = a * dqd + dt * Rd
+        q_new = qd + b * dq_new
+        dq, q = oracle.compress(dq_new, lay, pol), oracle.compress(q_new, lay, pol)
+        assert_words_match(tdq.cpu().numpy(), dq, lay, "SSS", f"stage {s} dq")
+        assert_words_match(tq.cpu().numpy(), q, lay, "SSS", f"stage {s} q")
+
+
+def test_rk_stage_f32_baseline(vc3b, cuda):
+    g = torch.Generator(device=cuda).manual_seed(3)
+    q, dq, R = (torch.rand(3 * 1001, device=cuda, generator=g) for _ in range(3))
+    q0, dq0 = q.clone(), dq.clone()
+    vc3b.ops.rk_stage_f32(0.5, 0.25, 1e-3, q, dq, R)
+    dq_ref = (torch.tensor(0.5, device=cuda) * dq0 + torch.tensor(1e-3, device=cuda) * R)
+    assert torch.equal(dq, dq_ref)
+    assert torch.equal(q, q0 + 0.25 * dq_ref)
