@@ -83,10 +83,6 @@ bool layout_ok(const vc3_layout& L) {
     return true;
 }
 
-long long floor_div_pow2(long long a, int shift) {  // floor(a / 2^shift)
-    return a >= 0 ? (a >> shift) : -((-a + (1LL << shift) - 1) >> shift);
-}
-
 // Host derivation of the by-value parameter block.  The double expressions
 // of the bucket arithmetic are the reference's (_kernels.py:139-140)
 // evaluated in IEEE double; the doubled forms are exact scalings of them.
@@ -97,11 +93,7 @@ Params make_params(const vc3_layout& L) {
     P.p = L.phi_bits;
     P.t = L.theta_bits;
     P.bias = L.exponent_bias;
-    P.emax = (1 << P.e) - 1;
-    P.ntmax = (1LL << P.t) - 1;
-    P.npmax = (1LL << P.p) - 1;
-    P.tmask = (unsigned long long)P.ntmax;
-    P.pmask = (unsigned long long)P.npmax;
+    derive_int_fields(P);
     const volatile double pi = kPi;  // keep host arithmetic plain IEEE double
     P.nt_half = (double)P.ntmax / 2.0;
     P.t_scale = (double)P.ntmax / (2.0 * pi);
@@ -109,30 +101,17 @@ Params make_params(const vc3_layout& L) {
     P.nt_half2 = 2.0 * P.nt_half;
     P.t_scale2 = 2.0 * P.t_scale;
     P.p_scale2 = 2.0 * P.p_scale;
-    P.field_low = 2u << P.m;
-    P.field_high = ((unsigned)(P.emax - 1) << P.m) | ((1u << P.m) - 1u);
-    // tools/exhaustive.cu: fused theta bucket == reference for every float32
-    // theta at widths 1..29 (t = 30 and 32 each have a handful of ties).
-    P.theta_fma = P.t <= 29;
-    // decode tables
-    P.table_mode = (P.t <= 20 && P.p <= 20) ? 1 : 0;
-    P.t_shift = P.t > 9 ? P.t - 9 : 0;
-    P.p_shift = P.p > 9 ? P.p - 9 : 0;
-    const long long half_t = P.t_shift ? (1LL << (P.t_shift - 1)) : 0;
-    const long long half_p = P.p_shift ? (1LL << (P.p_shift - 1)) : 0;
-    const long long lo_t = floor_div_pow2(-P.ntmax + half_t, P.t_shift);
-    const long long hi_t = floor_div_pow2(P.ntmax + half_t, P.t_shift);
-    P.t_off = (int)(-lo_t);
-    P.t_n = (int)(hi_t - lo_t + 1);
-    P.p_n = (int)(floor_div_pow2(P.npmax + half_p, P.p_shift) + 1);
-    P.p_base = P.t_n + 2;
-    P.tab_n = P.p_base + P.p_n + 1;
     const long double pid = (long double)kPi;
     P.t_delta = (double)(pid / (long double)P.ntmax);
     P.p_delta = (double)(pid / (long double)P.npmax);
     P.t_rcp = 1.0 / (double)P.ntmax;
     P.p_rcp = 1.0 / (double)P.npmax;
     return P;
+}
+
+bool is_default_layout(const vc3_layout& L) {
+    return L.sign_bits == 0 && L.exponent_bits == 7 && L.mantissa_bits == 22 && L.phi_bits == 17 &&
+           L.theta_bits == 18 && L.exponent_bias == 80;
 }
 
 // sin/cos(RN(pi) * k / b) to double accuracy: exact quarter-turn reduction,
@@ -255,11 +234,13 @@ __device__ __forceinline__ void load_table(double2* sm, const double2* __restric
 // ===================== kernels ==============================================
 
 // K1 compress: 4 vectors (48 B in, 32 B out) per thread per step.
-template <unsigned POLICY, bool NARROW>
+template <unsigned POLICY, bool NARROW, class LAY>
 __global__ void __launch_bounds__(kThreads) k_compress(const float* __restrict__ xyz,
                                                        unsigned long long* __restrict__ out,
-                                                       int64_t n, Params P, bool vec,
+                                                       int64_t n, Params Pin, bool vec,
                                                        int32_t* __restrict__ nonfinite) {
+    Params P = Pin;
+    LAY::apply(P);
     int bad = 0;
     const int64_t groups = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
@@ -283,11 +264,13 @@ __global__ void __launch_bounds__(kThreads) k_compress(const float* __restrict__
 }
 
 // K2 decompress: 4 words (32 B in, 48 B out) per thread per step.
-template <bool TABLE>
+template <bool TABLE, class LAY>
 __global__ void __launch_bounds__(kThreads) k_decompress(const unsigned long long* __restrict__ w,
                                                          float* __restrict__ xyz, int64_t n,
-                                                         Params P, bool vec,
+                                                         Params Pin, bool vec,
                                                          const double2* __restrict__ gtab) {
+    Params P = Pin;
+    LAY::apply(P);
     extern __shared__ double2 s_tab[];
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
@@ -325,12 +308,14 @@ __device__ __forceinline__ unsigned long long add_one(unsigned long long a, unsi
     return compress_one<POLICY, kFma, TABLE>(__fadd_rn(x1, x2), __fadd_rn(y1, y2), __fadd_rn(z1, z2), P);
 }
 
-template <unsigned POLICY, bool TABLE>
+template <unsigned POLICY, bool TABLE, class LAY>
 __global__ void __launch_bounds__(kThreads) k_add(const unsigned long long* __restrict__ a,
                                                   const unsigned long long* __restrict__ b,
                                                   unsigned long long* __restrict__ c, int64_t n,
-                                                  Params P, bool vec,
+                                                  Params Pin, bool vec,
                                                   const double2* __restrict__ gtab) {
+    Params P = Pin;
+    LAY::apply(P);
     extern __shared__ double2 s_tab[];
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
@@ -399,11 +384,13 @@ __device__ __forceinline__ unsigned long long axpy_one(float al, unsigned long l
                                       __fadd_rn(__fmul_rn(al, z1), z2), P);
 }
 
-template <unsigned POLICY, bool TABLE>
+template <unsigned POLICY, bool TABLE, class LAY>
 __global__ void __launch_bounds__(kThreads) k_axpy(float al, const unsigned long long* __restrict__ x,
                                                    const unsigned long long* y,
-                                                   unsigned long long* yo, int64_t n, Params P,
+                                                   unsigned long long* yo, int64_t n, Params Pin,
                                                    bool vec, const double2* __restrict__ gtab) {
+    Params P = Pin;
+    LAY::apply(P);
     extern __shared__ double2 s_tab[];
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
@@ -438,13 +425,15 @@ __device__ __forceinline__ void rk_one(float ca, float cb, float dt, unsigned lo
     q = compress_one<POLICY, kFma, TABLE>(q0, q1, q2, P);
 }
 
-template <unsigned POLICY, bool TABLE>
+template <unsigned POLICY, bool TABLE, class LAY>
 __global__ void __launch_bounds__(kThreads) k_rk(float ca, float cb, float dt,
                                                  unsigned long long* __restrict__ q,
                                                  unsigned long long* __restrict__ dq,
                                                  const unsigned long long* __restrict__ R,
-                                                 int64_t n, Params P, bool vec,
+                                                 int64_t n, Params Pin, bool vec,
                                                  const double2* __restrict__ gtab) {
+    Params P = Pin;
+    LAY::apply(P);
     extern __shared__ double2 s_tab[];
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
@@ -650,13 +639,16 @@ int by_policy(uint32_t pol, A... args) {
 
 template <unsigned POL>
 struct RunCompress {
-    static int run(const float* x, uint64_t* w, int64_t n, const Params& P, int32_t* nf, cudaStream_t s) {
+    static int run(const float* x, uint64_t* w, int64_t n, const Params& P, bool def, int32_t* nf,
+                   cudaStream_t s) {
         const bool vec = aligned16(x) && aligned16(w);
         const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
-        if (P.t <= 29 && P.p <= 29)
-            k_compress<POL, true><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
+        if (def)
+            k_compress<POL, true, DefaultLayout><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
+        else if (P.t <= 29 && P.p <= 29)
+            k_compress<POL, true, RuntimeLayout><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
         else
-            k_compress<POL, false><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
+            k_compress<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
         return launch_status();
     }
 };
@@ -664,15 +656,17 @@ struct RunCompress {
 template <unsigned POL>
 struct RunAdd {
     static int run(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t n, const Params& P,
-                   const double2* tab, cudaStream_t s) {
+                   bool def, const double2* tab, cudaStream_t s) {
         auto A = (const unsigned long long*)a, B = (const unsigned long long*)b;
         auto C = (unsigned long long*)c;
         const bool vec = aligned16(a) && aligned16(b) && aligned16(c);
         const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
-        if (P.table_mode)
-            k_add<POL, true><<<grid, kThreads, table_smem(P), s>>>(A, B, C, n, P, vec, tab);
+        if (def)
+            k_add<POL, true, DefaultLayout><<<grid, kThreads, table_smem(P), s>>>(A, B, C, n, P, vec, tab);
+        else if (P.table_mode)
+            k_add<POL, true, RuntimeLayout><<<grid, kThreads, table_smem(P), s>>>(A, B, C, n, P, vec, tab);
         else
-            k_add<POL, false><<<grid, kThreads, 0, s>>>(A, B, C, n, P, vec, tab);
+            k_add<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(A, B, C, n, P, vec, tab);
         return launch_status();
     }
 };
@@ -680,15 +674,17 @@ struct RunAdd {
 template <unsigned POL>
 struct RunAxpy {
     static int run(float al, const uint64_t* x, const uint64_t* y, uint64_t* yo, int64_t n,
-                   const Params& P, const double2* tab, cudaStream_t s) {
+                   const Params& P, bool def, const double2* tab, cudaStream_t s) {
         auto X = (const unsigned long long*)x, Y = (const unsigned long long*)y;
         auto O = (unsigned long long*)yo;
         const bool vec = aligned16(x) && aligned16(y) && aligned16(yo);
         const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
-        if (P.table_mode)
-            k_axpy<POL, true><<<grid, kThreads, table_smem(P), s>>>(al, X, Y, O, n, P, vec, tab);
+        if (def)
+            k_axpy<POL, true, DefaultLayout><<<grid, kThreads, table_smem(P), s>>>(al, X, Y, O, n, P, vec, tab);
+        else if (P.table_mode)
+            k_axpy<POL, true, RuntimeLayout><<<grid, kThreads, table_smem(P), s>>>(al, X, Y, O, n, P, vec, tab);
         else
-            k_axpy<POL, false><<<grid, kThreads, 0, s>>>(al, X, Y, O, n, P, vec, tab);
+            k_axpy<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(al, X, Y, O, n, P, vec, tab);
         return launch_status();
     }
 };
@@ -696,15 +692,17 @@ struct RunAxpy {
 template <unsigned POL>
 struct RunRk {
     static int run(float ca, float cb, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
-                   int64_t n, const Params& P, const double2* tab, cudaStream_t s) {
+                   int64_t n, const Params& P, bool def, const double2* tab, cudaStream_t s) {
         auto Q = (unsigned long long*)q, D = (unsigned long long*)dq;
         auto RR = (const unsigned long long*)R;
         const bool vec = aligned16(q) && aligned16(dq) && aligned16(R);
         const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
-        if (P.table_mode)
-            k_rk<POL, true><<<grid, kThreads, table_smem(P), s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
+        if (def)
+            k_rk<POL, true, DefaultLayout><<<grid, kThreads, table_smem(P), s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
+        else if (P.table_mode)
+            k_rk<POL, true, RuntimeLayout><<<grid, kThreads, table_smem(P), s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
         else
-            k_rk<POL, false><<<grid, kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
+            k_rk<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
         return launch_status();
     }
 };
@@ -751,8 +749,8 @@ int vc3_compress(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout
     if (policy > 7u) return VC3_ERR_ARG;
     VC3_CHECK_N(n);
     if (!xyz || !words) return VC3_ERR_ARG;
-    return by_policy<RunCompress>(policy, xyz, words, n, make_params(layout), d_nonfinite,
-                                  (cudaStream_t)stream);
+    return by_policy<RunCompress>(policy, xyz, words, n, make_params(layout),
+                                  is_default_layout(layout), d_nonfinite, (cudaStream_t)stream);
 }
 
 int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout, void* stream) {
@@ -767,10 +765,12 @@ int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layo
     const bool vec = aligned16(words) && aligned16(xyz);
     const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
     cudaStream_t s = (cudaStream_t)stream;
-    if (P.table_mode)
-        k_decompress<true><<<grid, kThreads, table_smem(P), s>>>(W, xyz, n, P, vec, tab);
+    if (is_default_layout(layout))
+        k_decompress<true, DefaultLayout><<<grid, kThreads, table_smem(P), s>>>(W, xyz, n, P, vec, tab);
+    else if (P.table_mode)
+        k_decompress<true, RuntimeLayout><<<grid, kThreads, table_smem(P), s>>>(W, xyz, n, P, vec, tab);
     else
-        k_decompress<false><<<grid, kThreads, 0, s>>>(W, xyz, n, P, vec, tab);
+        k_decompress<false, RuntimeLayout><<<grid, kThreads, 0, s>>>(W, xyz, n, P, vec, tab);
     return launch_status();
 }
 
@@ -784,7 +784,8 @@ int vc3_add_compressed(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_
     const double2* tab = nullptr;
     int st = get_table(P, &tab);
     if (st) return st;
-    return by_policy<RunAdd>(policy, a, b, c, n, P, tab, (cudaStream_t)stream);
+    return by_policy<RunAdd>(policy, a, b, c, n, P, is_default_layout(layout), tab,
+                             (cudaStream_t)stream);
 }
 
 int vc3_add_raw(const float* a, const float* b, float* c, int64_t n_floats, void* stream) {
@@ -806,7 +807,8 @@ int vc3_axpy(float alpha, const uint64_t* x, const uint64_t* y, uint64_t* y_out,
     const double2* tab = nullptr;
     int st = get_table(P, &tab);
     if (st) return st;
-    return by_policy<RunAxpy>(policy, alpha, x, y, y_out, n, P, tab, (cudaStream_t)stream);
+    return by_policy<RunAxpy>(policy, alpha, x, y, y_out, n, P, is_default_layout(layout), tab,
+                              (cudaStream_t)stream);
 }
 
 int vc3_rk_stage(float a, float b, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
@@ -819,7 +821,8 @@ int vc3_rk_stage(float a, float b, float dt, uint64_t* q, uint64_t* dq, const ui
     const double2* tab = nullptr;
     int st = get_table(P, &tab);
     if (st) return st;
-    return by_policy<RunRk>(policy, a, b, dt, q, dq, R, n, P, tab, (cudaStream_t)stream);
+    return by_policy<RunRk>(policy, a, b, dt, q, dq, R, n, P, is_default_layout(layout), tab,
+                            (cudaStream_t)stream);
 }
 
 int vc3_rk_stage_f32(float a, float b, float dt, float* q, float* dq, const float* R,
