@@ -14,7 +14,8 @@ from pathlib import Path
 
 from . import errors
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libvc3_b200.so"
+LIB_PATH = Path(os.environ.get("VC3_B200_LIB") or
+                (Path(__file__).resolve().parent / "lib" / "libvc3_b200.so"))
 
 
 class Layout(ctypes.Structure):

@@ -62,6 +62,15 @@ int sm_count() {
 }
 
 constexpr int kThreads = 256;
+// measured on B200 (tools/occupancy_sweep.py): 4 vectors per thread step and
+// >= 4 resident CTAs per SM (<= 64 registers) give the best fused-add issue rate
+#ifndef VC3_FUSED_MIN_BLOCKS
+#define VC3_FUSED_MIN_BLOCKS 4
+#endif
+#ifndef VC3_ADD_VPT
+#define VC3_ADD_VPT 4
+#endif
+
 
 // grid for `items` work items of one thread each: at most `per_sm` CTAs per
 // SM (grid-stride beyond that), at least one.
@@ -102,7 +111,7 @@ Params make_params(const vc3_layout& L) {
     P.t_scale2 = 2.0 * P.t_scale;
     P.p_scale2 = 2.0 * P.p_scale;
     const long double pid = (long double)kPi;
-    P.t_delta = (double)(pid / (long double)P.ntmax);
+    P.t_delta = (double)(2.0L * pid / (long double)P.ntmax);
     P.p_delta = (double)(pid / (long double)P.npmax);
     P.t_rcp = 1.0 / (double)P.ntmax;
     P.p_rcp = 1.0 / (double)P.npmax;
@@ -157,21 +166,20 @@ int get_table(const Params& P, const double2** out) {
         *out = it->second;
         return VC3_OK;
     }
-    // layout: [theta grid t_n][theta endpoints 2][phi grid p_n][phi pole 1]
+    // layout: [theta grid (t_n - 1)][theta endpoint nt = ntmax][phi grid (p_n - 1)][phi pole]
     std::vector<double2> h((size_t)P.tab_n);
-    for (int i = 0; i < P.t_n; ++i) {
+    for (int i = 0; i < P.t_n - 1; ++i) {
         double s, c;
-        sincos_host((long long)(i - P.t_off) << P.t_shift, P.ntmax, &s, &c);
+        sincos_host(2 * ((long long)i << P.t_shift) - P.ntmax, P.ntmax, &s, &c);
         h[i] = make_double2(s, c);
     }
-    h[P.t_n] = make_double2(-kPiTail, -1.0);     // nt = 0:     sin(-RN(pi)), cos(-RN(pi))
-    h[P.t_n + 1] = make_double2(kPiTail, -1.0);  // nt = ntmax: sin(+RN(pi)), cos(+RN(pi))
-    for (int i = 0; i < P.p_n; ++i) {
+    h[P.t_n - 1] = make_double2(kPiTail, -1.0);  // nt = ntmax: sin(+RN(pi)), cos(+RN(pi))
+    for (int i = 0; i < P.p_n - 1; ++i) {
         double s, c;
         sincos_host((long long)i << P.p_shift, P.npmax, &s, &c);
         h[P.p_base + i] = make_double2(s, c);
     }
-    h[P.p_base + P.p_n] = make_double2(0.0, -1.0);  // nph = npmax: the reference's exact pole
+    h[P.p_base + P.p_n - 1] = make_double2(0.0, -1.0);  // nph = npmax: the reference's exact pole
     double2* d = nullptr;
     int st = cuda_status(cudaMalloc((void**)&d, h.size() * sizeof(double2)));
     if (st) return st;
@@ -186,6 +194,30 @@ int get_table(const Params& P, const double2** out) {
 }
 
 size_t table_smem(const Params& P) { return P.table_mode ? (size_t)P.tab_n * sizeof(double2) : 0; }
+
+// Opt a kernel into more than 48 KB of dynamic shared memory (the default
+// layout's table is 49 KB), once per (device, kernel).
+int ensure_smem(const void* func, size_t bytes) {
+    if (bytes <= 48 * 1024) return VC3_OK;
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> done;
+    const auto key = std::make_pair(current_device(), func);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = done.find(key);
+    if (it != done.end() && it->second >= bytes) return VC3_OK;
+    const int st = cuda_status(
+        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    if (st == VC3_OK) done[key] = bytes;
+    return st;
+}
+
+// launch a table kernel: opt in to its shared-memory size first
+#define VC3_LAUNCH_TABLE(KERNEL, GRID, SMEM, STREAM, ...)                          \
+    do {                                                                           \
+        const int st_ = ensure_smem((const void*)(KERNEL), (SMEM));                \
+        if (st_) return st_;                                                       \
+        KERNEL<<<(GRID), kThreads, (SMEM), (STREAM)>>>(__VA_ARGS__);               \
+    } while (0)
 
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
@@ -235,7 +267,7 @@ __device__ __forceinline__ void load_table(double2* sm, const double2* __restric
 
 // K1 compress: 4 vectors (48 B in, 32 B out) per thread per step.
 template <unsigned POLICY, bool NARROW, class LAY>
-__global__ void __launch_bounds__(kThreads) k_compress(const float* __restrict__ xyz,
+__global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_compress(const float* __restrict__ xyz,
                                                        unsigned long long* __restrict__ out,
                                                        int64_t n, Params Pin, bool vec,
                                                        int32_t* __restrict__ nonfinite) {
@@ -265,7 +297,7 @@ __global__ void __launch_bounds__(kThreads) k_compress(const float* __restrict__
 
 // K2 decompress: 4 words (32 B in, 48 B out) per thread per step.
 template <bool TABLE, class LAY>
-__global__ void __launch_bounds__(kThreads) k_decompress(const unsigned long long* __restrict__ w,
+__global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_decompress(const unsigned long long* __restrict__ w,
                                                          float* __restrict__ xyz, int64_t n,
                                                          Params Pin, bool vec,
                                                          const double2* __restrict__ gtab) {
@@ -309,7 +341,7 @@ __device__ __forceinline__ unsigned long long add_one(unsigned long long a, unsi
 }
 
 template <unsigned POLICY, bool TABLE, class LAY>
-__global__ void __launch_bounds__(kThreads) k_add(const unsigned long long* __restrict__ a,
+__global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_add(const unsigned long long* __restrict__ a,
                                                   const unsigned long long* __restrict__ b,
                                                   unsigned long long* __restrict__ c, int64_t n,
                                                   Params Pin, bool vec,
@@ -320,13 +352,23 @@ __global__ void __launch_bounds__(kThreads) k_add(const unsigned long long* __re
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
-    const int64_t pairs = vec ? n / 2 : 0;
-    for (int64_t g = gtid(); g < pairs; g += gstride()) {
-        const ulonglong2 u = ld_stream_u2(a + 2 * g), v = ld_stream_u2(b + 2 * g);
-        st_u2(c + 2 * g, add_one<POLICY, TABLE>(u.x, v.x, P, tt, tp),
-              add_one<POLICY, TABLE>(u.y, v.y, P, tt, tp));
+    // VC3_ADD_VPT vectors per thread step (16-byte loads/stores of word pairs):
+    // independent vectors give the scheduler ILP across the long FP64 chains
+    constexpr int kV = VC3_ADD_VPT;
+    const int64_t groups = vec ? n / kV : 0;
+    for (int64_t g = gtid(); g < groups; g += gstride()) {
+        ulonglong2 u[kV / 2], v[kV / 2];
+#pragma unroll
+        for (int k = 0; k < kV / 2; ++k) {
+            u[k] = ld_stream_u2(a + kV * g + 2 * k);
+            v[k] = ld_stream_u2(b + kV * g + 2 * k);
+        }
+#pragma unroll
+        for (int k = 0; k < kV / 2; ++k)
+            st_u2(c + kV * g + 2 * k, add_one<POLICY, TABLE>(u[k].x, v[k].x, P, tt, tp),
+                  add_one<POLICY, TABLE>(u[k].y, v[k].y, P, tt, tp));
     }
-    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride())
+    for (int64_t i = groups * kV + gtid(); i < n; i += gstride())
         c[i] = add_one<POLICY, TABLE>(a[i], b[i], P, tt, tp);
 }
 
@@ -660,11 +702,11 @@ struct RunAdd {
         auto A = (const unsigned long long*)a, B = (const unsigned long long*)b;
         auto C = (unsigned long long*)c;
         const bool vec = aligned16(a) && aligned16(b) && aligned16(c);
-        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
+        const unsigned grid = grid_for(vec ? (n + VC3_ADD_VPT - 1) / VC3_ADD_VPT : n);
         if (def)
-            k_add<POL, true, DefaultLayout><<<grid, kThreads, table_smem(P), s>>>(A, B, C, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_add<POL, true, DefaultLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab);
         else if (P.table_mode)
-            k_add<POL, true, RuntimeLayout><<<grid, kThreads, table_smem(P), s>>>(A, B, C, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_add<POL, true, RuntimeLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab);
         else
             k_add<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(A, B, C, n, P, vec, tab);
         return launch_status();
@@ -680,9 +722,9 @@ struct RunAxpy {
         const bool vec = aligned16(x) && aligned16(y) && aligned16(yo);
         const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
         if (def)
-            k_axpy<POL, true, DefaultLayout><<<grid, kThreads, table_smem(P), s>>>(al, X, Y, O, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_axpy<POL, true, DefaultLayout>), grid, table_smem(P), s, al, X, Y, O, n, P, vec, tab);
         else if (P.table_mode)
-            k_axpy<POL, true, RuntimeLayout><<<grid, kThreads, table_smem(P), s>>>(al, X, Y, O, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_axpy<POL, true, RuntimeLayout>), grid, table_smem(P), s, al, X, Y, O, n, P, vec, tab);
         else
             k_axpy<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(al, X, Y, O, n, P, vec, tab);
         return launch_status();
@@ -698,9 +740,9 @@ struct RunRk {
         const bool vec = aligned16(q) && aligned16(dq) && aligned16(R);
         const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
         if (def)
-            k_rk<POL, true, DefaultLayout><<<grid, kThreads, table_smem(P), s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_rk<POL, true, DefaultLayout>), grid, table_smem(P), s, ca, cb, dt, Q, D, RR, n, P, vec, tab);
         else if (P.table_mode)
-            k_rk<POL, true, RuntimeLayout><<<grid, kThreads, table_smem(P), s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_rk<POL, true, RuntimeLayout>), grid, table_smem(P), s, ca, cb, dt, Q, D, RR, n, P, vec, tab);
         else
             k_rk<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
         return launch_status();
@@ -766,9 +808,9 @@ int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layo
     const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
     cudaStream_t s = (cudaStream_t)stream;
     if (is_default_layout(layout))
-        k_decompress<true, DefaultLayout><<<grid, kThreads, table_smem(P), s>>>(W, xyz, n, P, vec, tab);
+        VC3_LAUNCH_TABLE((k_decompress<true, DefaultLayout>), grid, table_smem(P), s, W, xyz, n, P, vec, tab);
     else if (P.table_mode)
-        k_decompress<true, RuntimeLayout><<<grid, kThreads, table_smem(P), s>>>(W, xyz, n, P, vec, tab);
+        VC3_LAUNCH_TABLE((k_decompress<true, RuntimeLayout>), grid, table_smem(P), s, W, xyz, n, P, vec, tab);
     else
         k_decompress<false, RuntimeLayout><<<grid, kThreads, 0, s>>>(W, xyz, n, P, vec, tab);
     return launch_status();

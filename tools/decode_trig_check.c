@@ -140,6 +140,20 @@ static void sincos_tab1(int64_t a, int64_t b, int sh, double* s, double* c) {
     *c = fma(-sA, sps, fma(cA, cm1, cA));
 }
 
+// Variant D (product since round 1b): plain bit split, index = n >> sh,
+// residual = n & (2^sh - 1) >= 0.  theta entry h: RN(pi)*(2h*2^sh - N)/N,
+// residual angle lo*RN(2 RN(pi)/N); phi entry h: RN(pi)*h*2^sh/NP.
+static void sincos_tabD(int64_t k_entry, int64_t b, int64_t lo, double delta, double* s, double* c) {
+    double sA, cA;
+    sincos_ld(k_entry, b, &sA, &cA);
+    double psi = (double)lo * delta;
+    double u = psi * psi;
+    double sps = fma(psi * u, fma(u, 1.0 / 120.0, -1.0 / 6.0), psi);
+    double cm1 = u * fma(u, 1.0 / 24.0, -0.5);
+    *s = fma(cA, sps, fma(sA, cm1, sA));
+    *c = fma(-sA, sps, fma(cA, cm1, cA));
+}
+
 static uint64_t rng_state = 0x9E3779B97F4A7C15ull;
 static uint64_t rng(void) { rng_state ^= rng_state << 13; rng_state ^= rng_state >> 7; rng_state ^= rng_state << 17; return rng_state; }
 
@@ -151,7 +165,7 @@ static int e2e(void) {
     for (int64_t n = 0; n <= NP; ++n) { double ph = PI_ * (double)n / (double)NP; sp[n] = sin(ph); cp[n] = cos(ph); }
     sp[NP] = 0.0; cp[NP] = -1.0;
     double rN = 1.0 / (double)N, rNP = 1.0 / (double)NP;
-    int64_t total = 0, misA = 0, misB = 0, misC = 0;
+    int64_t total = 0, misA = 0, misB = 0, misC = 0, misD = 0;
     for (int64_t i = 0; i < 20000000; ++i) {
         if ((i & 3) == 0) { /* force endpoints sometimes */ }
         uint64_t w = rng();
@@ -176,6 +190,16 @@ static int e2e(void) {
         if (nph == NP) { spC = 0; cpC = -1; } else sincos_tab1(nph, NP, 9, &spC, &cpC);
         float C[3] = {(float)(R * cC * spC), (float)(R * sC * spC), (float)(R * cpC)};
         for (int k = 0; k < 3; ++k) misC += C[k] != ref[k];
+        {
+            double sD, cD, spD, cpD;
+            const double dt2 = (double)(2.0L * (long double)PI_ / (long double)N), dp = (double)((long double)PI_ / (long double)NP);
+            if (nt == N) { sD = 1.2246467991473532e-16; cD = -1.0; }
+            else sincos_tabD(2 * ((nt >> 7) << 7) - N, N, nt & 127, dt2, &sD, &cD);
+            if (nph == NP) { spD = 0; cpD = -1; }
+            else sincos_tabD((nph >> 7) << 7, NP, nph & 127, dp, &spD, &cpD);
+            float D[3] = {(float)(R * cD * spD), (float)(R * sD * spD), (float)(R * cpD)};
+            for (int k = 0; k < 3; ++k) misD += D[k] != ref[k];
+        }
         float A[3] = {(float)(R * cA * spA), (float)(R * sA * spA), (float)(R * cpA)};
         float B[3] = {(float)(R * cB * spB), (float)(R * sB * spB), (float)(R * cpB)};
         for (int k = 0; k < 3; ++k) {
@@ -186,7 +210,7 @@ static int e2e(void) {
             (void)dA; (void)dB;
         }
     }
-    printf("variant C (table) mismatches %lld\n", (long long)misC);
+    printf("variant C (table) mismatches %lld, variant D (plain split table) %lld\n", (long long)misC, (long long)misD);
     printf("components %lld: variant A mismatches %lld (%.3g), variant B mismatches %lld (%.3g)\n",
            (long long)total, (long long)misA, (double)misA / total, (long long)misB, (double)misB / total);
     return 0;
@@ -234,6 +258,22 @@ int main(int argc, char** argv) {
                 }
             }
             hprint("C table1 sin", &hs); hprint("C table1 cos", &hc);
+        }
+        {
+            hist_t hs = {0}, hc = {0};
+            const int sh = t > 11 ? t - 11 : 0;
+            const double dlt = (double)(2.0L * (long double)PI_ / (long double)N);
+            for (int64_t n = 0; n <= N; ++n) {
+                double th = PI_ * (2.0 * (double)n / (double)N - 1.0);
+                double s2, c2;
+                if (n == N) { s2 = 1.2246467991473532e-16; c2 = -1.0; }
+                else {
+                    int64_t hi = n >> sh, lo = n & ((1LL << sh) - 1);
+                    sincos_tabD(2 * (hi << sh) - N, N, lo, dlt, &s2, &c2);
+                }
+                hadd(&hs, s2, sin(th)); hadd(&hc, c2, cos(th));
+            }
+            hprint("D theta sin", &hs); hprint("D theta cos", &hc);
         }
         hprint("A int-reduce sin", &hsA); hprint("A int-reduce cos", &hcA);
         hprint("B ref-angle sin", &hsB); hprint("B ref-angle cos", &hcB);
