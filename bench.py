@@ -45,14 +45,17 @@ BYTES_RAW = 36          # read two float3 + write one (bench.py:26)
 CPU_SAMPLE = 1 << 22    # vectors per CPU-baseline step
 
 
-def workload_config(n: int, world: int) -> dict:
+def workload_config(n: int, world: int, scaling: str = "weak", global_n: int | None = None) -> dict:
     return {
-        "workload": "C2 compressed vector add c=a+b (fused decompress-add-recompress), "
-                    "float3 cube vectors U[-1,1]^3, all-single policy, layout <0,7,22>-17-18@80",
+        "workload": ("C2 compressed vector add c=a+b (fused decompress-add-recompress), "
+                     "float3 cube vectors U[-1,1]^3, all-single policy, layout <0,7,22>-17-18@80"
+                     if scaling == "weak" else
+                     "C5 strong scaling: the C2 fused add on a fixed global array split into "
+                     "contiguous shards"),
         "n_vectors_per_gpu": n,
-        "global_vectors": n * world,
+        "global_vectors": global_n if global_n is not None else n * world,
         "bytes_per_vector": BYTES_COMPRESSED,
-        "l2": "working set 6 GiB per GPU >> 126 MB L2; no flush needed",
+        "l2": "working set >= 6 GiB per GPU >> 126 MB L2; no flush needed",
         "parallelism": f"shard{world} (contiguous, no collective)",
     }
 
@@ -159,6 +162,7 @@ def dist_setup(args):
 def run_reference(args, world, rank):
     if rank != 0:
         return
+    sample = args.cpu_sample
     sys.path.insert(0, str(ROOT / "oracle"))
     import vc3_oracle
 
@@ -166,8 +170,8 @@ def run_reference(args, world, rank):
 
     threads = vc3_oracle.default_threads()
     g = np.random.Generator(np.random.Philox(key=(0, 0)))
-    va = g.uniform(-1.0, 1.0, (CPU_SAMPLE, 3)).astype(np.float32)
-    vb = g.uniform(-1.0, 1.0, (CPU_SAMPLE, 3)).astype(np.float32)
+    va = g.uniform(-1.0, 1.0, (sample, 3)).astype(np.float32)
+    vb = g.uniform(-1.0, 1.0, (sample, 3)).astype(np.float32)
     a = vc3_oracle.compress(va, DEFAULT_LAYOUT, ALL_SINGLE_POLICY, threads)
     b = vc3_oracle.compress(vb, DEFAULT_LAYOUT, ALL_SINGLE_POLICY, threads)
     for _ in range(args.warmup):
@@ -176,14 +180,14 @@ def run_reference(args, world, rank):
     for _ in range(args.steps):
         vc3_oracle.add_compressed(a, b, DEFAULT_LAYOUT, ALL_SINGLE_POLICY, threads)
     dt = (time.perf_counter() - t0) / args.steps
-    value = CPU_SAMPLE / dt / 1e9
+    value = sample / dt / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": workload_config(N_PER_GPU, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{CPU_SAMPLE} cube vectors per step (bounded sample of the "
+                         "sample": f"{sample} cube vectors per step (bounded sample of the "
                                    f"2^28-vector workload), oracle/vc3_oracle.c add_compressed "
                                    f"on {threads} host threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -194,7 +198,7 @@ def run_reference(args, world, rank):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def cpu_baseline_sample() -> dict:
+def cpu_baseline_sample(sample: int = CPU_SAMPLE) -> dict:
     sys.path.insert(0, str(ROOT / "oracle"))
     import vc3_oracle
 
@@ -202,8 +206,8 @@ def cpu_baseline_sample() -> dict:
 
     threads = vc3_oracle.default_threads()
     g = np.random.Generator(np.random.Philox(key=(0, 1)))
-    va = g.uniform(-1.0, 1.0, (CPU_SAMPLE, 3)).astype(np.float32)
-    vb = g.uniform(-1.0, 1.0, (CPU_SAMPLE, 3)).astype(np.float32)
+    va = g.uniform(-1.0, 1.0, (sample, 3)).astype(np.float32)
+    vb = g.uniform(-1.0, 1.0, (sample, 3)).astype(np.float32)
     a = vc3_oracle.compress(va, DEFAULT_LAYOUT, ALL_SINGLE_POLICY, threads)
     b = vc3_oracle.compress(vb, DEFAULT_LAYOUT, ALL_SINGLE_POLICY, threads)
     vc3_oracle.add_compressed(a, b, DEFAULT_LAYOUT, ALL_SINGLE_POLICY, threads)
@@ -212,8 +216,8 @@ def cpu_baseline_sample() -> dict:
     for _ in range(reps):
         vc3_oracle.add_compressed(a, b, DEFAULT_LAYOUT, ALL_SINGLE_POLICY, threads)
     dt = (time.perf_counter() - t0) / reps
-    return {"value": CPU_SAMPLE / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{reps} x {CPU_SAMPLE} cube vectors, oracle/vc3_oracle.c add_compressed, "
+    return {"value": sample / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{reps} x {sample} cube vectors, oracle/vc3_oracle.c add_compressed, "
                       f"{threads} threads, after 1 warm-up pass"}
 
 
@@ -319,7 +323,16 @@ def run_gpu(args, world, rank, local):
     torch.cuda.set_device(dev)
     _native.load()
     lay, pol = vc3b.DEFAULT_LAYOUT, vc3b.ALL_SINGLE_POLICY
-    n = args.n
+    if args.scaling == "strong":
+        # C5: a fixed global problem split into contiguous shards
+        from paper_2003_02633_b200.analysis import shard_range
+
+        lo, hi = shard_range(args.total, rank, world)
+        n = hi - lo
+        global_n = args.total
+    else:
+        n = args.n
+        global_n = n * world
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -374,7 +387,7 @@ def run_gpu(args, world, rank, local):
         ms, clocks = timed(args.steps)
         remeasured = True
     ms_all = max_over_ranks(ms)
-    value = n * world / (ms_all * 1e-3) / 1e9
+    value = global_n / (ms_all * 1e-3) / 1e9
 
     # uncompressed float32 baseline on the same GPU (same vectors, 36 B/vec)
     ra = va.reshape(-1)
@@ -389,7 +402,7 @@ def run_gpu(args, world, rank, local):
     torch.cuda.synchronize()
     barrier()
     raw_ms = max_over_ranks(time_region(step_raw, args.steps, stream, torch))
-    raw_value = n * world / (raw_ms * 1e-3) / 1e9
+    raw_value = global_n / (raw_ms * 1e-3) / 1e9
 
     # secondary kernels (compress / decompress) for the roofline table
     out_v = torch.empty_like(va)
@@ -409,7 +422,7 @@ def run_gpu(args, world, rank, local):
     del out_v
 
     # e2e: public host-array API, pinned host buffers, copies inside the region
-    e2e_n = n
+    e2e_n = min(n, N_PER_GPU)  # pinned host staging bounded at one 2^28 shard
     ha = torch.empty(e2e_n, dtype=torch.uint64, pin_memory=True)
     hb = torch.empty(e2e_n, dtype=torch.uint64, pin_memory=True)
     ha.copy_(a[:e2e_n])
@@ -431,25 +444,27 @@ def run_gpu(args, world, rank, local):
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
     e2e_value = e2e_n * world / e2e_s / 1e9
     step_add()  # c was reused by the compress timing; recompute and cross-check e2e output
-    if not np.array_equal(hc, c.cpu().numpy()):
+    if not np.array_equal(hc, c[:e2e_n].cpu().numpy()):
         raise RuntimeError("host-API result differs from the device kernel result")
 
-    secondary_configs = {} if args.no_secondary else run_secondary(args, vc3b, lib, dev, stream, n)
+    # secondary configs are single-GPU characterisations; scaling runs skip them
+    secondary_configs = ({} if (args.no_secondary or world > 1)
+                         else run_secondary(args, vc3b, lib, dev, stream, min(n, N_PER_GPU)))
 
     peak, peak_src = measured_peak()
     achieved = BYTES_COMPRESSED * n / (ms * 1e-3) / 1e9
     traffic = ncu_traffic()
     if rank != 0:
         return
-    cpu = cpu_baseline_sample() if world == 1 else None
+    cpu = cpu_baseline_sample(args.cpu_sample) if world == 1 else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_all, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": workload_config(n, world),
-        "hbm_gb_s": BYTES_COMPRESSED * n * world / (ms_all * 1e-3) / 1e9,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(n, world, args.scaling, global_n),
+        "hbm_gb_s": BYTES_COMPRESSED * global_n / (ms_all * 1e-3) / 1e9,
         "fp32_add": {"value": raw_value, "unit": UNIT,
-                     "hbm_gb_s": BYTES_RAW * n * world / (raw_ms * 1e-3) / 1e9,
+                     "hbm_gb_s": BYTES_RAW * global_n / (raw_ms * 1e-3) / 1e9,
                      "ms_per_step": raw_ms},
         "speedup_vs_fp32_add": value / raw_value,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -480,6 +495,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=N_PER_GPU, help="vectors per GPU")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: --n vectors per GPU (C2); strong: --total split over GPUs (C5)")
+    ap.add_argument("--total", type=int, default=1 << 31, help="global vectors for --scaling strong")
+    ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE,
+                    help="vectors per CPU-baseline / reference-arm step")
     ap.add_argument("--no-secondary", action="store_true",
                     help="skip the C3/C4 secondary configs (quick runs)")
     args = ap.parse_args()

@@ -1,0 +1,25 @@
+"""bench.py contract checks that run without a GPU: the reference arm (the C
+port of the reference's CPU path) prints one valid JSON line."""
+
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_reference_arm_prints_contract_line():
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--steps", "2", "--warmup", "1", "--cpu-sample", "65536"],
+                         capture_output=True, text=True, check=True, timeout=600)
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference"
+    assert d["unit"] == "Gvec/s" and d["higher_is_better"] is True and d["value"] > 0
+    assert d["warmup"] >= 3  # the contract's minimum warm-up is enforced
+    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    assert d["e2e"] == {"value": d["value"], "unit": "Gvec/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}
+    assert d["metric"].startswith("compressed float3 vector-add")
