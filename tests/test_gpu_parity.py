@@ -398,3 +398,24 @@ def test_rk_stage_f32_baseline(vc3b, cuda):
     dq_ref = (torch.tensor(0.5, device=cuda) * dq0 + torch.tensor(1e-3, device=cuda) * R)
     assert torch.equal(dq, dq_ref)
     assert torch.equal(q, q0 + 0.25 * dq_ref)
+
+
+@pytest.mark.parametrize("lname", ["base_16_16", "wide_10_25", "17_17"])
+@pytest.mark.parametrize("code", ["SSS", "SDS"])
+def test_fused_ops_other_layouts_vs_oracle(vc3b, oracle, cuda, lname, code):
+    """Fused add / axpy on the generic-layout kernels (runtime layout, and the
+    reference-angle decode for the 25-bit theta layout) against the oracle."""
+    lay, pol = layout_by_name(lname), policy_by_code(code)
+    g = np.random.Generator(np.random.Philox(key=(len(lname), 9)))
+    n = 20_001
+    va = (g.normal(size=(n, 3)) * 10.0 ** g.uniform(-4, 4, (n, 1))).astype(np.float32)
+    vb = g.uniform(-1, 1, (n, 3)).astype(np.float32)
+    a, b = oracle.compress(va, lay, pol), oracle.compress(vb, lay, pol)
+    ta, tb = torch.from_numpy(a).to(cuda), torch.from_numpy(b).to(cuda)
+    assert_words_match(vc3b.add_compressed(ta, tb, lay, pol).cpu().numpy(),
+                       oracle.add_compressed(a, b, lay, pol), lay, code, f"add {lname}")
+    al = np.float32(0.73)
+    assert_words_match(vc3b.axpy(al, ta, tb, lay, pol).cpu().numpy(),
+                       oracle.axpy(al, a, b, lay, pol), lay, code, f"axpy {lname}")
+    assert_vectors_match(vc3b.decompress(ta, lay).cpu().numpy(), oracle.decompress(a, lay),
+                         f"decompress {lname}")
