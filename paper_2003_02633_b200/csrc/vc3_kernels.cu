@@ -335,8 +335,8 @@ __device__ __forceinline__ unsigned long long add_one(unsigned long long a, unsi
                                                       const Params& P, const double2* tt,
                                                       const double2* tp) {
     float x1, y1, z1, x2, y2, z2;
-    decompress_one<TABLE>(a, P, tt, tp, x1, y1, z1);
-    decompress_one<TABLE>(b, P, tt, tp, x2, y2, z2);
+    decompress_one<TABLE, true>(a, P, tt, tp, x1, y1, z1);
+    decompress_one<TABLE, true>(b, P, tt, tp, x2, y2, z2);
     return compress_one<POLICY, kFma, TABLE>(__fadd_rn(x1, x2), __fadd_rn(y1, y2), __fadd_rn(z1, z2), P);
 }
 
@@ -419,8 +419,8 @@ __device__ __forceinline__ unsigned long long axpy_one(float al, unsigned long l
                                                        unsigned long long y, const Params& P,
                                                        const double2* tt, const double2* tp) {
     float x1, y1, z1, x2, y2, z2;
-    decompress_one<TABLE>(x, P, tt, tp, x1, y1, z1);
-    decompress_one<TABLE>(y, P, tt, tp, x2, y2, z2);
+    decompress_one<TABLE, true>(x, P, tt, tp, x1, y1, z1);
+    decompress_one<TABLE, true>(y, P, tt, tp, x2, y2, z2);
     return compress_one<POLICY, kFma, TABLE>(__fadd_rn(__fmul_rn(al, x1), x2),
                                       __fadd_rn(__fmul_rn(al, y1), y2),
                                       __fadd_rn(__fmul_rn(al, z1), z2), P);
@@ -454,9 +454,9 @@ __device__ __forceinline__ void rk_one(float ca, float cb, float dt, unsigned lo
                                        unsigned long long& dq, unsigned long long r,
                                        const Params& P, const double2* tt, const double2* tp) {
     float q0, q1, q2, d0, d1, d2, r0, r1, r2;
-    decompress_one<TABLE>(q, P, tt, tp, q0, q1, q2);
-    decompress_one<TABLE>(dq, P, tt, tp, d0, d1, d2);
-    decompress_one<TABLE>(r, P, tt, tp, r0, r1, r2);
+    decompress_one<TABLE, true>(q, P, tt, tp, q0, q1, q2);
+    decompress_one<TABLE, true>(dq, P, tt, tp, d0, d1, d2);
+    decompress_one<TABLE, true>(r, P, tt, tp, r0, r1, r2);
     d0 = __fadd_rn(__fmul_rn(ca, d0), __fmul_rn(dt, r0));
     d1 = __fadd_rn(__fmul_rn(ca, d1), __fmul_rn(dt, r1));
     d2 = __fadd_rn(__fmul_rn(ca, d2), __fmul_rn(dt, r2));

@@ -59,6 +59,17 @@ __global__ void k_theta(unsigned lo, unsigned hi, Params P, unsigned long long* 
     }
 }
 
+__global__ void k_sqrt(unsigned lo, unsigned hi, unsigned long long* bad, unsigned* first) {
+    for (unsigned long long b = lo + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+         b <= hi; b += (unsigned long long)gridDim.x * blockDim.x) {
+        const float x = __uint_as_float((unsigned)b);
+        if (__float_as_uint(sqrt_rn_normal(x)) != __float_as_uint(__fsqrt_rn(x))) {
+            atomicAdd(bad, 1ull);
+            atomicMin(first, (unsigned)b);
+        }
+    }
+}
+
 static Params params_for_t(int t) {
     Params P = {};
     P.t = t;
@@ -112,6 +123,11 @@ int main() {
     run("acos_f32[w in -0..-1]", 0x80000000u, NEG_ONE,
         [&](unsigned lo, unsigned hi, auto bad, auto first) {
             k_acos<<<grid, block>>>(lo, hi, bad, first);
+        });
+    // branch-free sqrt on acos_f32's argument range [2^-25, 0.25]
+    run("sqrt_rn_normal[x in 2^-25..0.25]", 0x33000000u, 0x3E800000u,
+        [&](unsigned lo, unsigned hi, auto bad, auto first) {
+            k_sqrt<<<grid, block>>>(lo, hi, bad, first);
         });
     for (int t = 1; t <= 32; ++t) {
         // the kernels use the fused theta form only for t <= 29 (Params::theta_fma)
