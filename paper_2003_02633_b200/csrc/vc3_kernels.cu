@@ -275,9 +275,17 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_compress(con
     LAY::apply(P);
     int bad = 0;
     const int64_t groups = vec ? n / 4 : 0;
-    for (int64_t g = gtid(); g < groups; g += gstride()) {
-        const float* src = xyz + 12 * g;
-        const float4 a = ld_stream_f4(src), b = ld_stream_f4(src + 4), c = ld_stream_f4(src + 8);
+    int64_t g = gtid();
+    float4 an = make_float4(0, 0, 0, 0), bn = an, cn = an;
+    if (g < groups) {
+        an = ld_stream_f4(xyz + 12 * g); bn = ld_stream_f4(xyz + 12 * g + 4); cn = ld_stream_f4(xyz + 12 * g + 8);
+    }
+    for (; g < groups; g += gstride()) {
+        const float4 a = an, b = bn, c = cn;
+        const int64_t gn = g + gstride();
+        if (gn < groups) {
+            an = ld_stream_f4(xyz + 12 * gn); bn = ld_stream_f4(xyz + 12 * gn + 4); cn = ld_stream_f4(xyz + 12 * gn + 8);
+        }
         bad += !finite3(a.x, a.y, a.z) + !finite3(a.w, b.x, b.y) + !finite3(b.z, b.w, c.x) +
                !finite3(c.y, c.z, c.w);
         const unsigned long long w0 = compress_one<POLICY, kFma, NARROW>(a.x, a.y, a.z, P);
@@ -308,8 +316,15 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_decompress(c
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
     const int64_t groups = vec ? n / 4 : 0;
-    for (int64_t g = gtid(); g < groups; g += gstride()) {
-        const ulonglong2 u = ld_stream_u2(w + 4 * g), v = ld_stream_u2(w + 4 * g + 2);
+    // register double buffering: the next step's words are in flight while
+    // this step decodes (one CTA holds only 1024 threads at 49 KB of table)
+    int64_t g = gtid();
+    ulonglong2 un = make_ulonglong2(0, 0), vn = un;
+    if (g < groups) { un = ld_stream_u2(w + 4 * g); vn = ld_stream_u2(w + 4 * g + 2); }
+    for (; g < groups; g += gstride()) {
+        const ulonglong2 u = un, v = vn;
+        const int64_t gn = g + gstride();
+        if (gn < groups) { un = ld_stream_u2(w + 4 * gn); vn = ld_stream_u2(w + 4 * gn + 2); }
         float o[12];
         decompress_one<TABLE>(u.x, P, tt, tp, o[0], o[1], o[2]);
         decompress_one<TABLE>(u.y, P, tt, tp, o[3], o[4], o[5]);
