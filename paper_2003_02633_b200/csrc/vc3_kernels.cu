@@ -67,6 +67,9 @@ constexpr int kThreads = 256;
 #ifndef VC3_FUSED_MIN_BLOCKS
 #define VC3_FUSED_MIN_BLOCKS 4
 #endif
+#ifndef VC3_DECOMP_STAGE
+#define VC3_DECOMP_STAGE 1
+#endif
 #ifndef VC3_ADD_VPT
 #define VC3_ADD_VPT 4
 #endif
@@ -275,6 +278,9 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_compress(con
     LAY::apply(P);
     int bad = 0;
     const int64_t groups = vec ? n / 4 : 0;
+    // (shared-memory staging of this input was measured slower: the kernel
+    // is issue-bound, so the 16-byte strided loads stay; the next step's
+    // loads are issued before this step's compute)
     int64_t g = gtid();
     float4 an = make_float4(0, 0, 0, 0), bn = an, cn = an;
     if (g < groups) {
@@ -316,12 +322,21 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_decompress(c
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
     const int64_t groups = vec ? n / 4 : 0;
+#if VC3_DECOMP_STAGE
+    // per-warp shared staging of the array-of-structs output: each lane's 48 B
+    // go to shared memory, then the warp writes 3 x 512 contiguous bytes
+    float4* stage = reinterpret_cast<float4*>(s_tab + (TABLE ? P.tab_n : 0)) + (threadIdx.x >> 5) * 96;
+    const int lane = threadIdx.x & 31;
+#endif
     // register double buffering: the next step's words are in flight while
     // this step decodes (one CTA holds only 1024 threads at 49 KB of table)
     int64_t g = gtid();
     ulonglong2 un = make_ulonglong2(0, 0), vn = un;
     if (g < groups) { un = ld_stream_u2(w + 4 * g); vn = ld_stream_u2(w + 4 * g + 2); }
-    for (; g < groups; g += gstride()) {
+    // whole warps step together so the staged stores stay warp-uniform
+    const int64_t gw_end = ((groups + 31) / 32) * 32;
+    for (; g < gw_end; g += gstride()) {
+        const bool live = g < groups;
         const ulonglong2 u = un, v = vn;
         const int64_t gn = g + gstride();
         if (gn < groups) { un = ld_stream_u2(w + 4 * gn); vn = ld_stream_u2(w + 4 * gn + 2); }
@@ -330,10 +345,30 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_decompress(c
         decompress_one<TABLE>(u.y, P, tt, tp, o[3], o[4], o[5]);
         decompress_one<TABLE>(v.x, P, tt, tp, o[6], o[7], o[8]);
         decompress_one<TABLE>(v.y, P, tt, tp, o[9], o[10], o[11]);
-        float* dst = xyz + 12 * g;
-        st_f4(dst, o[0], o[1], o[2], o[3]);
-        st_f4(dst + 4, o[4], o[5], o[6], o[7]);
-        st_f4(dst + 8, o[8], o[9], o[10], o[11]);
+#if VC3_DECOMP_STAGE
+        stage[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
+        stage[3 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
+        stage[3 * lane + 2] = make_float4(o[8], o[9], o[10], o[11]);
+        __syncwarp();
+        const int64_t g0 = g - lane;  // first group of this warp
+        float* base = xyz + 12 * g0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int idx = 32 * k + lane;  // float4 index within the warp's 1536 B
+            if (g0 + idx / 3 < groups) {
+                const float4 f = stage[idx];
+                st_f4(base + 4 * idx, f.x, f.y, f.z, f.w);
+            }
+        }
+        __syncwarp();
+#else
+        if (live) {
+            float* dst = xyz + 12 * g;
+            st_f4(dst, o[0], o[1], o[2], o[3]);
+            st_f4(dst + 4, o[4], o[5], o[6], o[7]);
+            st_f4(dst + 8, o[8], o[9], o[10], o[11]);
+        }
+#endif
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float x, y, z;
@@ -822,12 +857,13 @@ int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layo
     const bool vec = aligned16(words) && aligned16(xyz);
     const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
     cudaStream_t s = (cudaStream_t)stream;
+    const size_t stage = VC3_DECOMP_STAGE ? (size_t)kThreads * 48 : 0;  // 1.5 KB per warp
     if (is_default_layout(layout))
-        VC3_LAUNCH_TABLE((k_decompress<true, DefaultLayout>), grid, table_smem(P), s, W, xyz, n, P, vec, tab);
+        VC3_LAUNCH_TABLE((k_decompress<true, DefaultLayout>), grid, table_smem(P) + stage, s, W, xyz, n, P, vec, tab);
     else if (P.table_mode)
-        VC3_LAUNCH_TABLE((k_decompress<true, RuntimeLayout>), grid, table_smem(P), s, W, xyz, n, P, vec, tab);
+        VC3_LAUNCH_TABLE((k_decompress<true, RuntimeLayout>), grid, table_smem(P) + stage, s, W, xyz, n, P, vec, tab);
     else
-        k_decompress<false, RuntimeLayout><<<grid, kThreads, 0, s>>>(W, xyz, n, P, vec, tab);
+        VC3_LAUNCH_TABLE((k_decompress<false, RuntimeLayout>), grid, stage, s, W, xyz, n, P, vec, tab);
     return launch_status();
 }
 
