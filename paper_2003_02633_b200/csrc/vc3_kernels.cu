@@ -70,9 +70,6 @@ constexpr int kThreads = 256;
 #ifndef VC3_DECOMP_STAGE
 #define VC3_DECOMP_STAGE 1
 #endif
-#ifndef VC3_ADD_VPT
-#define VC3_ADD_VPT 4
-#endif
 
 
 // grid for `items` work items of one thread each: at most `per_sm` CTAs per
@@ -223,6 +220,7 @@ int ensure_smem(const void* func, size_t bytes) {
     } while (0)
 
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+inline bool aligned32(const void* p) { return ((uintptr_t)p & 31u) == 0; }
 
 // ----- streaming loads/stores (read-once data: keep it out of L1) ----------
 __device__ __forceinline__ ulonglong2 ld_stream_u2(const unsigned long long* p) {
@@ -238,6 +236,24 @@ __device__ __forceinline__ float4 ld_stream_f4(const float* p) {
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "l"(p));
     return v;
+}
+// sm_100 256-bit global accesses (LDG/STG .256): four words per instruction
+struct u64x4 {
+    unsigned long long x, y, z, w;
+};
+__device__ __forceinline__ u64x4 ld_stream_u4(const unsigned long long* p) {
+    u64x4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(v.x), "=l"(v.y), "=l"(v.z), "=l"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_u4(unsigned long long* p, unsigned long long a,
+                                      unsigned long long b, unsigned long long c,
+                                      unsigned long long d) {
+    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
+                 "l"(d)
+                 : "memory");
 }
 __device__ __forceinline__ void st_u2(unsigned long long* p, unsigned long long a,
                                       unsigned long long b) {
@@ -298,8 +314,7 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_compress(con
         const unsigned long long w1 = compress_one<POLICY, kFma, NARROW>(a.w, b.x, b.y, P);
         const unsigned long long w2 = compress_one<POLICY, kFma, NARROW>(b.z, b.w, c.x, P);
         const unsigned long long w3 = compress_one<POLICY, kFma, NARROW>(c.y, c.z, c.w, P);
-        st_u2(out + 4 * g, w0, w1);
-        st_u2(out + 4 * g + 2, w2, w3);
+        st_u4(out + 4 * g, w0, w1, w2, w3);
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         const float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
@@ -331,20 +346,20 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_decompress(c
     // register double buffering: the next step's words are in flight while
     // this step decodes (one CTA holds only 1024 threads at 49 KB of table)
     int64_t g = gtid();
-    ulonglong2 un = make_ulonglong2(0, 0), vn = un;
-    if (g < groups) { un = ld_stream_u2(w + 4 * g); vn = ld_stream_u2(w + 4 * g + 2); }
+    u64x4 wn = {0, 0, 0, 0};
+    if (g < groups) wn = ld_stream_u4(w + 4 * g);
     // whole warps step together so the staged stores stay warp-uniform
     const int64_t gw_end = ((groups + 31) / 32) * 32;
     for (; g < gw_end; g += gstride()) {
         const bool live = g < groups;
-        const ulonglong2 u = un, v = vn;
+        const u64x4 u = wn;
         const int64_t gn = g + gstride();
-        if (gn < groups) { un = ld_stream_u2(w + 4 * gn); vn = ld_stream_u2(w + 4 * gn + 2); }
+        if (gn < groups) wn = ld_stream_u4(w + 4 * gn);
         float o[12];
         decompress_one<TABLE>(u.x, P, tt, tp, o[0], o[1], o[2]);
         decompress_one<TABLE>(u.y, P, tt, tp, o[3], o[4], o[5]);
-        decompress_one<TABLE>(v.x, P, tt, tp, o[6], o[7], o[8]);
-        decompress_one<TABLE>(v.y, P, tt, tp, o[9], o[10], o[11]);
+        decompress_one<TABLE>(u.z, P, tt, tp, o[6], o[7], o[8]);
+        decompress_one<TABLE>(u.w, P, tt, tp, o[9], o[10], o[11]);
 #if VC3_DECOMP_STAGE
         stage[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
         stage[3 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
@@ -402,21 +417,17 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_add(const un
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
-    // VC3_ADD_VPT vectors per thread step (16-byte loads/stores of word pairs):
-    // independent vectors give the scheduler ILP across the long FP64 chains
-    constexpr int kV = VC3_ADD_VPT;
+    // four independent vectors per thread step give the scheduler ILP across
+    // the long FP64 chains; words move with sm_100 256-bit accesses
+    constexpr int kV = 4;  // one 32-byte load per operand and one 32-byte store per step
     const int64_t groups = vec ? n / kV : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
-        ulonglong2 u[kV / 2], v[kV / 2];
-#pragma unroll
-        for (int k = 0; k < kV / 2; ++k) {
-            u[k] = ld_stream_u2(a + kV * g + 2 * k);
-            v[k] = ld_stream_u2(b + kV * g + 2 * k);
-        }
-#pragma unroll
-        for (int k = 0; k < kV / 2; ++k)
-            st_u2(c + kV * g + 2 * k, add_one<POLICY, TABLE>(u[k].x, v[k].x, P, tt, tp),
-                  add_one<POLICY, TABLE>(u[k].y, v[k].y, P, tt, tp));
+        const u64x4 u = ld_stream_u4(a + kV * g), v = ld_stream_u4(b + kV * g);
+        const unsigned long long c0 = add_one<POLICY, TABLE>(u.x, v.x, P, tt, tp);
+        const unsigned long long c1 = add_one<POLICY, TABLE>(u.y, v.y, P, tt, tp);
+        const unsigned long long c2 = add_one<POLICY, TABLE>(u.z, v.z, P, tt, tp);
+        const unsigned long long c3 = add_one<POLICY, TABLE>(u.w, v.w, P, tt, tp);
+        st_u4(c + kV * g, c0, c1, c2, c3);
     }
     for (int64_t i = groups * kV + gtid(); i < n; i += gstride())
         c[i] = add_one<POLICY, TABLE>(a[i], b[i], P, tt, tp);
@@ -733,7 +744,7 @@ template <unsigned POL>
 struct RunCompress {
     static int run(const float* x, uint64_t* w, int64_t n, const Params& P, bool def, int32_t* nf,
                    cudaStream_t s) {
-        const bool vec = aligned16(x) && aligned16(w);
+        const bool vec = aligned16(x) && aligned32(w);
         const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
         if (def)
             k_compress<POL, true, DefaultLayout><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
@@ -751,8 +762,8 @@ struct RunAdd {
                    bool def, const double2* tab, cudaStream_t s) {
         auto A = (const unsigned long long*)a, B = (const unsigned long long*)b;
         auto C = (unsigned long long*)c;
-        const bool vec = aligned16(a) && aligned16(b) && aligned16(c);
-        const unsigned grid = grid_for(vec ? (n + VC3_ADD_VPT - 1) / VC3_ADD_VPT : n);
+        const bool vec = aligned32(a) && aligned32(b) && aligned32(c);
+        const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
         if (def)
             VC3_LAUNCH_TABLE((k_add<POL, true, DefaultLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab);
         else if (P.table_mode)
@@ -854,7 +865,7 @@ int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layo
     int st = get_table(P, &tab);
     if (st) return st;
     auto W = (const unsigned long long*)words;
-    const bool vec = aligned16(words) && aligned16(xyz);
+    const bool vec = aligned32(words) && aligned16(xyz);
     const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
     cudaStream_t s = (cudaStream_t)stream;
     const size_t stage = VC3_DECOMP_STAGE ? (size_t)kThreads * 48 : 0;  // 1.5 KB per warp
