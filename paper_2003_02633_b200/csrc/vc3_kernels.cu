@@ -351,7 +351,6 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_decompress(c
     // whole warps step together so the staged stores stay warp-uniform
     const int64_t gw_end = ((groups + 31) / 32) * 32;
     for (; g < gw_end; g += gstride()) {
-        const bool live = g < groups;
         const u64x4 u = wn;
         const int64_t gn = g + gstride();
         if (gn < groups) wn = ld_stream_u4(w + 4 * gn);
