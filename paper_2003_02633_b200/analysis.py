@@ -217,3 +217,69 @@ from .variants import (  # noqa: E402,F401
     joint_encode,
     split_sweep,
 )
+
+
+# ---------------------------------------------------------------------------
+# characterisation studies on the device path
+# ---------------------------------------------------------------------------
+def _angle_bits(words, layout):
+    w = words.view(torch.int64)
+    nt = w & layout.n_theta_max
+    nph = (w >> layout.theta_bits) & layout.n_phi_max
+    return nt, nph
+
+
+def bin_miss_study(domain: SampleDomain, layout=DEFAULT_LAYOUT) -> tuple[float, float]:
+    """Fraction of samples whose theta / phi bucket differs between the
+    all-single and all-double pipelines (analysis.py:236-254).  Both bucket
+    sets come from the compress kernel (its angle bits are exactly
+    quantize_angles(to_spherical(v)) for every nonzero vector; zero vectors
+    give equal buckets in both pipelines, as in the reference)."""
+    from .layout import ALL_SINGLE_POLICY, ORACLE_POLICY
+
+    if domain.count == 0:
+        raise EmptyDomain("bin_miss_study needs at least one sample")
+    layout = as_layout(layout)
+    miss_t = miss_p = 0
+    for i in range(domain.n_chunks()):
+        v = _dev.upload(domain.chunk(i, domain.chunk_size(i)))
+        ts, ps = _angle_bits(compress(v, layout, ALL_SINGLE_POLICY), layout)
+        td, pd = _angle_bits(compress(v, layout, ORACLE_POLICY), layout)
+        miss_t += int((ts != td).sum().item())
+        miss_p += int((ps != pd).sum().item())
+    return miss_t / domain.count, miss_p / domain.count
+
+
+@dataclass
+class IdempotenceResult:
+    word_miss_fraction: float
+    predicted_bound: float
+    third_cycle_stable_fraction: float
+    count: int
+
+    def to_dict(self) -> dict:
+        return {"word_miss_fraction": self.word_miss_fraction,
+                "predicted_bound": self.predicted_bound,
+                "third_cycle_stable_fraction": self.third_cycle_stable_fraction,
+                "count": self.count}
+
+
+def idempotence_study(domain: SampleDomain, layout=DEFAULT_LAYOUT, policy=DEFAULT_POLICY,
+                      u: int = 8) -> IdempotenceResult:
+    """Word stability under repeated compress/decompress cycles
+    (analysis.py:446-486): miss = compress(decompress(w1)) != w1."""
+    if domain.count == 0:
+        raise EmptyDomain("idempotence_study needs at least one sample")
+    layout, policy = as_layout(layout), as_policy(policy)
+    misses = stable3 = 0
+    for i in range(domain.n_chunks()):
+        v = _dev.upload(domain.chunk(i, domain.chunk_size(i)))
+        w1 = compress(v, layout, policy)
+        w2 = compress(decompress(w1, layout), layout, policy)
+        w3 = compress(decompress(w2, layout), layout, policy)
+        misses += int((w1.view(torch.int64) != w2.view(torch.int64)).sum().item())
+        stable3 += int((w2.view(torch.int64) == w3.view(torch.int64)).sum().item())
+    m_int = 24 if (policy.theta_single or policy.phi_single) else 53
+    p_eff = max(layout.phi_bits, layout.theta_bits)
+    bound = 2.0 * u * 2.0 ** (p_eff - m_int)
+    return IdempotenceResult(misses / domain.count, bound, stable3 / domain.count, domain.count)

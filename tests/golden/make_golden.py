@@ -234,6 +234,27 @@ def main():
     rows = analysis.split_sweep(35, splits, analysis.SampleDomain("unit_sphere", 100_000, 7))
     d["split_study"] = np.array([[st.mean, st.max, st.stddev, st.count] for _, st in rows])
 
+    # characterisation studies (analysis.py:236-254, 446-486)
+    d["binmiss_sphere"] = np.array(analysis.bin_miss_study(
+        analysis.SampleDomain("unit_sphere", 300_000, 3)))
+    d["binmiss_cube"] = np.array(analysis.bin_miss_study(analysis.SampleDomain("cube", 300_000, 3)))
+    for pname in ("SDS", "DDD", "SSS"):
+        r = analysis.idempotence_study(analysis.SampleDomain("unit_sphere", 300_000, 4),
+                                       DEFAULT_LAYOUT, ALL_POLICIES[pname])
+        d[f"idem_{pname}"] = np.array([r.word_miss_fraction, r.predicted_bound,
+                                       r.third_cycle_stable_fraction, r.count])
+
+    # VC3C stream bytes (stream.py:1-87) and CSV text
+    import io as _io
+    from vc3 import stream as _stream
+    for lname in ("17_18", "base_16_16"):
+        buf = _io.BytesIO()
+        _stream.write_stream(buf, d[f"cw_{lname}_SSS_kat"], LAYOUTS[lname])
+        d[f"stream_{lname}"] = np.frombuffer(buf.getvalue(), dtype=np.uint8)
+    sbuf = _io.StringIO()
+    _stream.write_csv(sbuf, edge)
+    d["csv_edge"] = np.frombuffer(sbuf.getvalue().encode(), dtype=np.uint8)
+
     np.savez_compressed(OUT / "golden.npz", **d)
     total = sum(v.nbytes for v in d.values())
     print(f"wrote {len(d)} arrays ({total / 1e6:.1f} MB raw) to {OUT / 'golden.npz'}")

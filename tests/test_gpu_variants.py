@@ -137,3 +137,23 @@ def test_variants_larger_vs_oracle(vc3b, oracle, cuda):
     assert same.mean() > 0.999
     out = variants.decompress_variant(torch.from_numpy(w2).to(cuda), cfg, lay).cpu().numpy()
     assert_vectors_match(out[same], vh2[same], "split 98304")
+
+
+def test_bin_miss_and_idempotence_studies_match_reference(golden, vc3b, cuda):
+    """the characterisation studies on the device path."""
+    from paper_2003_02633_b200 import analysis
+
+    for kind in ("sphere", "cube"):
+        dom = analysis.SampleDomain("unit_sphere" if kind == "sphere" else "cube", 300_000, 3)
+        mt, mp = analysis.bin_miss_study(dom)
+        ref = golden[f"binmiss_{kind}"]
+        # CUDA vs glibc double atan2/acos can move a handful of tie samples
+        assert abs(mt - ref[0]) * dom.count <= 3 and abs(mp - ref[1]) * dom.count <= 3
+    for code, pol in (("SDS", vc3b.DEFAULT_POLICY), ("DDD", vc3b.ORACLE_POLICY),
+                      ("SSS", vc3b.ALL_SINGLE_POLICY)):
+        r = analysis.idempotence_study(analysis.SampleDomain("unit_sphere", 300_000, 4),
+                                       vc3b.DEFAULT_LAYOUT, pol)
+        ref = golden[f"idem_{code}"]
+        assert r.count == int(ref[3]) and r.predicted_bound == ref[1]
+        assert abs(r.word_miss_fraction - ref[0]) * r.count <= 2
+        assert abs(r.third_cycle_stable_fraction - ref[2]) * r.count <= 2
