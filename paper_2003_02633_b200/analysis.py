@@ -25,7 +25,16 @@ from . import _dev, _native
 from ._dev import torch
 from .codec import compress, decompress
 from .errors import EmptyDomain
-from .layout import DEFAULT_LAYOUT, DEFAULT_POLICY, as_layout, as_policy
+from .layout import (  # noqa: F401  (the reference's analysis namespace)
+    ALL_SINGLE_POLICY,
+    DEFAULT_LAYOUT,
+    DEFAULT_POLICY,
+    ORACLE_POLICY,
+    BitLayout,
+    PrecisionPolicy,
+    as_layout,
+    as_policy,
+)
 
 CHUNK = 1 << 20   # analysis.py:29
 
@@ -283,3 +292,95 @@ def idempotence_study(domain: SampleDomain, layout=DEFAULT_LAYOUT, policy=DEFAUL
     p_eff = max(layout.phi_bits, layout.theta_bits)
     bound = 2.0 * u * 2.0 ** (p_eff - m_int)
     return IdempotenceResult(misses / domain.count, bound, stable3 / domain.count, domain.count)
+
+
+def precision_comparison(count: int, seed: int, layout=DEFAULT_LAYOUT) -> list[dict]:
+    """Normalised error statistics for the four theta/phi single/double
+    policies (quantisation single) on the unit sphere and the cube
+    (analysis.py:170-191); each row is one device ``error_study``."""
+    from .layout import PrecisionPolicy
+
+    rows = []
+    for kind in ("unit_sphere", "cube"):
+        domain = SampleDomain(kind, count, seed)
+        for theta in ("single", "double"):
+            for phi in ("single", "double"):
+                st = error_study(domain, layout, PrecisionPolicy(theta, phi, "single"),
+                                 normalised=True)
+                rows.append({"domain": kind, "theta": theta, "phi": phi, **st.to_dict()})
+    return rows
+
+
+def anisotropy_map(layout=DEFAULT_LAYOUT, policy=None, grid: tuple[int, int] = (32, 16),
+                   count: int = 1_000_000, seed: int = 0):
+    """Mean round-trip error per (theta, phi) cell of the unit sphere
+    (analysis.py:194-223): (means, counts, theta_edges, phi_edges), NaN in
+    empty cells.  Round trip, errors and cell binning all run on the device
+    (float64 atan2/acos for the cell of the *input* vector, as the
+    reference); cell sums accumulate with index_add in float64."""
+    from .layout import ORACLE_POLICY
+
+    tc, pc = grid
+    if tc < 1 or pc < 1:
+        raise ValueError("grid cells must be >= 1")
+    layout = as_layout(layout)
+    policy = as_policy(ORACLE_POLICY if policy is None else policy)
+    domain = SampleDomain("unit_sphere", count, seed)
+    _dev.require_torch_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sums = torch.zeros(tc * pc, dtype=torch.float64, device=dev)
+    counts = torch.zeros(tc * pc, dtype=torch.int64, device=dev)
+    for i in range(domain.n_chunks()):
+        v = _dev.upload(domain.chunk(i, domain.chunk_size(i)))
+        vh = decompress(compress(v, layout, policy), layout)
+        v64 = v.to(torch.float64)
+        d = v64 - vh.to(torch.float64)
+        e = torch.sqrt((d * d).sum(dim=1))
+        x, y, z = v64.unbind(1)
+        r = torch.sqrt(x * x + y * y + z * z)
+        th = torch.atan2(y, x)
+        ph = torch.acos(torch.clamp(z / torch.where(r > 0, r, torch.ones_like(r)), -1.0, 1.0))
+        ti = torch.clamp(((th + math.pi) / (2 * math.pi) * tc).to(torch.int64), 0, tc - 1)
+        pj = torch.clamp((ph / math.pi * pc).to(torch.int64), 0, pc - 1)
+        cell = ti * pc + pj
+        sums.index_add_(0, cell, e)
+        counts.index_add_(0, cell, torch.ones_like(cell))
+    sums = sums.reshape(tc, pc).cpu().numpy()
+    counts = counts.reshape(tc, pc).cpu().numpy()
+    means = np.where(counts > 0, sums / np.maximum(counts, 1), np.nan)
+    return (means, counts, np.linspace(-np.pi, np.pi, tc + 1), np.linspace(0.0, np.pi, pc + 1))
+
+
+def anisotropy_rows(means: np.ndarray) -> list[tuple[int, int, float]]:
+    """(theta_cell, phi_cell, mean) for every non-empty cell (analysis.py:226-233)."""
+    return [(i, j, float(means[i, j])) for i in range(means.shape[0])
+            for j in range(means.shape[1]) if not np.isnan(means[i, j])]
+
+
+def smith_theta_bins(phi: float, n_phi_max: int, tau: float) -> int:
+    """Azimuth bins on the ring at ``phi`` that keep the chordal error within
+    ``tau`` (the variable-bin comparison rule of analysis.py:420-443; host
+    scalar arithmetic, no fixed-rate code uses it)."""
+    from .errors import DomainError
+
+    if not 0.0 < phi < math.pi:
+        raise DomainError("phi must lie strictly inside (0, pi)")
+    if tau <= 0:
+        raise DomainError("tau must be positive")
+    half_ring = math.pi / (2.0 * n_phi_max)
+    c = (math.cos(tau) - math.cos(phi) * math.cos(phi + half_ring)) / (
+        math.sin(phi) * math.sin(phi + half_ring))
+    if not -1.0 <= c <= 1.0:
+        raise DomainError(f"arccos argument {c} outside [-1, 1]")
+    width = math.acos(c)
+    if width == 0.0:
+        raise DomainError("tolerance exactly at the ring spacing limit")
+    return int(math.ceil(math.pi / width))
+
+
+def report(domain: SampleDomain, layout, policy, **extra) -> dict:
+    """The studies' machine-readable envelope (analysis.py:489-500)."""
+    doc = {"layout": str(as_layout(layout)), "policy": as_policy(policy).spec(),
+           "domain": domain.describe(), "seed": domain.seed, "count": domain.count}
+    doc.update(extra)
+    return doc

@@ -255,6 +255,16 @@ def main():
     _stream.write_csv(sbuf, edge)
     d["csv_edge"] = np.frombuffer(sbuf.getvalue().encode(), dtype=np.uint8)
 
+    # anisotropy map, precision comparison, Smith bins (analysis.py:170-233, 420-443)
+    means, counts, _, _ = analysis.anisotropy_map(DEFAULT_LAYOUT, ORACLE_POLICY, (8, 4), 200_000, 3)
+    d["aniso_means"], d["aniso_counts"] = means, counts
+    rows = analysis.precision_comparison(100_000, 1)
+    d["prec_cmp"] = np.array([[r["mean"], r["max"], r["stddev"], r["count"]] for r in rows])
+    smith = []
+    for phi, npm, tau in ((0.3, 64, 0.05), (1.5, 1000, 0.01), (2.9, 131071, 1e-4), (1.0, 8, 0.5)):
+        smith.append(analysis.smith_theta_bins(phi, npm, tau))
+    d["smith_bins"] = np.array(smith)
+
     np.savez_compressed(OUT / "golden.npz", **d)
     total = sum(v.nbytes for v in d.values())
     print(f"wrote {len(d)} arrays ({total / 1e6:.1f} MB raw) to {OUT / 'golden.npz'}")

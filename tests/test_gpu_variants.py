@@ -157,3 +157,24 @@ def test_bin_miss_and_idempotence_studies_match_reference(golden, vc3b, cuda):
         assert r.count == int(ref[3]) and r.predicted_bound == ref[1]
         assert abs(r.word_miss_fraction - ref[0]) * r.count <= 2
         assert abs(r.third_cycle_stable_fraction - ref[2]) * r.count <= 2
+
+
+def test_anisotropy_and_precision_comparison_match_reference(golden, vc3b, cuda):
+    """analysis.py:170-233 on the device path."""
+    from paper_2003_02633_b200 import analysis
+
+    means, counts, te, pe = analysis.anisotropy_map(vc3b.DEFAULT_LAYOUT, vc3b.ORACLE_POLICY,
+                                                    (8, 4), 200_000, 3)
+    # cell of the input vector: CUDA vs numpy float64 atan2/acos may move a
+    # sample sitting on a cell edge; none did at this seed
+    assert np.abs(counts - golden["aniso_counts"]).sum() <= 2
+    np.testing.assert_allclose(means, golden["aniso_means"], rtol=1e-6)
+    assert te.size == 9 and pe.size == 5
+    rows = analysis.anisotropy_rows(means)
+    assert len(rows) == 32 and rows[0][:2] == (0, 0)
+    got = analysis.precision_comparison(100_000, 1)
+    ref = golden["prec_cmp"]
+    assert [(r["domain"], r["theta"], r["phi"]) for r in got][:2] == [
+        ("unit_sphere", "single", "single"), ("unit_sphere", "single", "double")]
+    arr = np.array([[r["mean"], r["max"], r["stddev"], r["count"]] for r in got])
+    np.testing.assert_allclose(arr, ref, rtol=1e-6)
