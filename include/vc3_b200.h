@@ -168,6 +168,28 @@ int vc3_variant_maxima(vc3_layout layout, vc3_variant variant, int64_t* n_theta_
 int vc3_error_stats(const float* v, const float* vh, int64_t n, int32_t normalised,
                     int64_t chunk, double* d_chunk_stats, void* stream);
 
+/* ---- flux-reconstruction flux divergence (Alg. 1) ------
+ * No reference code exists; the operation is the paper's
+ * Algorithm 1 for step 10 of its FR table:
+ *   div[(k*n_vars + c)*ld + i] = sum_j sum_d D[(d*n_points + j)*n_points + k]
+ *                                * X_d(words[(j*n_vars + c)*ld + i])
+ * with X = decompress(word) (vc3_decompress), D the 3*n_points x n_points
+ * divergence operator (float32, row-major, device memory), i < n_elem the
+ * element, c < n_vars the equation, n_points <= 256 solution points per
+ * element and ld >= n_elem the element stride.  Runs on the tcgen05 tensor
+ * cores with fp32-accurate operand splitting (3xTF32).
+ *
+ * vc3_fr_prepare_operator splits D into the kernel's staged operator
+ * (vc3_fr_operator_floats(n_points) floats of device memory, 16-B aligned);
+ * prepare once per operator, reuse for every call. */
+int64_t vc3_fr_operator_floats(int n_points);
+int vc3_fr_prepare_operator(const float* D, int n_points, float* op, void* stream);
+int vc3_fr_divergence(const uint64_t* words, const float* op, float* div, int64_t n_elem,
+                      int n_vars, int64_t ld, int n_points, vc3_layout layout, void* stream);
+/* Uncompressed baseline: flux[((j*n_vars + c)*ld + i)*3 + d] float32. */
+int vc3_fr_divergence_f32(const float* flux, const float* op, float* div, int64_t n_elem,
+                          int n_vars, int64_t ld, int n_points, void* stream);
+
 /* ---- host-buffer entry points (reference-facing, synchronous) ------------
  * Same operations on HOST arrays: the call streams chunks host->device, runs
  * the kernel and copies results back, overlapping copies and compute on

@@ -17,8 +17,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libvc3_b200.so"
-SOURCES = ["vc3_kernels.cu", "vc3_host.cu", "vc3_variants.cu"]
-HEADERS = ["vc3_device.cuh"]
+SOURCES = ["vc3_kernels.cu", "vc3_host.cu", "vc3_variants.cu", "vc3_fr.cu"]
+HEADERS = ["vc3_device.cuh", "vc3_rt.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NUMERICS = ["-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true"]

@@ -1,0 +1,464 @@
+// vc3_fr.cu — flux-reconstruction flux divergence on compressed fluxes
+// (Alg. 1), on the sm_100a tensor cores.
+//
+//   div[k][c][i] = sum_j sum_d D[d*ns + j][k] * X[j][c][i][d],
+//   X[j][c][i] = decompress(words[(j*n_vars + c)*ld + i])      (a 3-vector)
+//
+// i = element, c = equation (variable), j/k = solution points, d = dimension.
+// For each equation this is a GEMM  Out_c (n_elem x ns) = A_c (n_elem x 3ns)
+// * D' (3ns x ns), with the decode of the compressed flux as the producer of
+// the A operand.  At k = 4 (ns = 125) it is 93,750 flops per element-equation
+// against 1,500 B of compressed input and output — beyond the FP32 CUDA-core
+// rate at HBM speed — so the contraction runs on tcgen05:
+//
+//  * one CTA per tile of 128 elements of one equation; 8 decode warps, one
+//    operator-load warp (cp.async.bulk of the pre-split operator slice from
+//    L2), one MMA warp (a single elected thread issues tcgen05.mma);
+//  * K is walked in stages of 8 solution points (24 k-values): the decode
+//    warps write the stage's A slice straight into shared memory in the
+//    canonical no-swizzle K-major UMMA layout (8-row x 16-byte core
+//    matrices), the MMA warp accumulates into TMEM (128 lanes x Npad fp32
+//    columns), stages ring through NST buffers guarded by mbarriers;
+//  * fp32 accuracy on TF32 tensor cores by operand splitting (3xTF32):
+//    a = a_hi + a_lo, b = b_hi + b_lo with a_hi the top 19 bits, and
+//    a*b ~ a_hi*b_hi + a_hi*b_lo + a_lo*b_hi (relative error ~2^-21);
+//  * epilogue: tcgen05.ld of the accumulator (lane = element, column = k),
+//    coalesced 128-byte stores per output point.
+//
+// The uncompressed baseline (float32 [j][c][i][3] fluxes) runs the same
+// kernel with plain loads in place of the decode.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/vc3_b200.h"
+#include "vc3_device.cuh"
+#include "vc3_rt.h"
+
+using namespace vc3;
+using namespace vc3::rt;
+
+namespace {
+
+constexpr int kRows = 256;             // elements per tile: two UMMA M = 128 halves
+constexpr int kHalf = 128;
+constexpr int kPts = 8;                // solution points per K stage
+constexpr int kDecodeWarps = 16;       // 2 threads per element, 4 points each
+constexpr int kThreadsFr = (kDecodeWarps + 2) * 32;
+constexpr int kLoadWarp = kDecodeWarps;
+constexpr int kMmaWarp = kDecodeWarps + 1;
+constexpr int kASliceBytes = kHalf * kPts * 4;  // one half, one dimension, hi or lo: 4 KB
+
+__host__ __device__ constexpr int b_slice_bytes(int npad) { return npad * kPts * 4; }
+// stage: A slices [hi|lo][half m][dimension d] (12 x 4 KB), then B slices
+// [hi|lo][d] (6 x npad x 32 B)
+__host__ __device__ constexpr int stage_bytes(int npad) {
+    return 12 * kASliceBytes + 6 * b_slice_bytes(npad);
+}
+__host__ __device__ constexpr int a_slice(int lo, int m, int d) { return ((lo * 2 + m) * 3 + d) * kASliceBytes; }
+
+// ---- PTX wrappers -----------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// canonical no-swizzle K-major shared-memory matrix descriptor (sm_100 format:
+// start>>4 [0,14), LBO>>4 [16,30), SBO>>4 [32,46), version 1 [46,48), layout 0)
+__device__ __forceinline__ uint64_t smem_desc(const void* p, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((smem_u32(p) & 0x3FFFFu) >> 4) | ((uint64_t)(lbo >> 4) << 16) |
+           ((uint64_t)(sbo >> 4) << 32) | (1ull << 46);
+}
+// instruction descriptor: D f32, A/B tf32, both K-major, M = 128, N = npad
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = __uint_as_float(r[q]);
+}
+
+__device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
+
+// offset of (row, kk) inside one canonical K-major slice of 8 k-values:
+// core matrices of 8 rows x 16 B; LBO (next 4 k-values) = 128 B, SBO (next
+// 8 rows) = 256 B
+__host__ __device__ constexpr int canon_off(int row, int kk) {
+    return (row >> 3) * 256 + (kk >> 2) * 128 + (row & 7) * 16 + (kk & 3) * 4;
+}
+
+// ---- operator preparation -----------------------------------------------------
+// Bprep[s][hi|lo][d][canonical npad x 8] from D[3ns][ns] (row d*ns + j, column k)
+__global__ void k_fr_prepare(const float* __restrict__ D, int ns, int npad, int nst,
+                             float* __restrict__ out) {
+    const int per_stage = 6 * npad * kPts;
+    const int total = nst * per_stage;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+        const int s = idx / per_stage;
+        int r = idx - s * per_stage;
+        const int part = r / (npad * kPts);  // 0..2 hi d0..d2, 3..5 lo d0..d2
+        r -= part * npad * kPts;
+        const int n = r / kPts, kk = r - n * kPts;
+        const int d = part % 3;
+        const int j = s * kPts + kk;
+        const float v = (j < ns && n < ns) ? D[(size_t)(d * ns + j) * ns + n] : 0.0f;
+        const float hi = tf32_hi(v);
+        out[(size_t)s * per_stage + part * npad * kPts + canon_off(n, kk) / 4] = part < 3 ? hi : v - hi;
+    }
+}
+
+// ---- the fused kernel -----------------------------------------------------------
+struct FrArgs {
+    const unsigned long long* words;  // compressed fluxes [ns][n_vars][ld]
+    const float* raw;                 // or float32 fluxes [ns][n_vars][ld][3]
+    const float* bprep;               // k_fr_prepare output
+    float* out;                       // [ns][n_vars][ld]
+    int64_t n_elem, ld;
+    int n_vars, ns, npad, nst, nbuf;
+};
+
+template <bool RAW, bool TABLE, class LAY>
+__global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, const double2* __restrict__ gtab) {
+    Params P = Pin;
+    LAY::apply(P);
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int sbytes = stage_bytes(a.npad);
+    unsigned char* stages = smem;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)a.nbuf * sbytes);
+    uint64_t* empty = full + a.nbuf;
+    uint64_t* accum_full = empty + a.nbuf;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
+    double2* s_tab = reinterpret_cast<double2*>(smem + (size_t)a.nbuf * sbytes + 1024);
+    const uint32_t tmem_cols = 2 * a.npad <= 256 ? 256 : 512;
+
+    const int64_t tiles_per_var = (a.n_elem + kRows - 1) / kRows;
+    const int c = (int)(blockIdx.x / tiles_per_var);
+    const int64_t i0 = (blockIdx.x - (int64_t)c * tiles_per_var) * kRows;
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < a.nbuf; ++b) {
+            mbar_init(&full[b], kDecodeWarps + 1);
+            mbar_init(&empty[b], 1);
+        }
+        mbar_init(accum_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (!RAW && TABLE) {
+        for (int t = threadIdx.x; t < P.tab_n; t += blockDim.x) s_tab[t] = gtab[t];
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < kDecodeWarps) {
+        // ---------------- producers of A (decode) ----------------
+        const int row = threadIdx.x & (kRows - 1), h = threadIdx.x / kRows;
+        const int m = row / kHalf;
+        const int64_t i = i0 + row;
+        const bool live = i < a.n_elem;
+        const double2* tt = s_tab;
+        const double2* tp = s_tab + P.p_base;
+        const int64_t plane = (int64_t)a.n_vars * a.ld;  // stride between solution points
+        const int64_t base = (int64_t)c * a.ld + i + (int64_t)(4 * h) * plane;
+        const int64_t plane2 = 2 * plane, plane3 = 3 * plane, step = (int64_t)kPts * plane;
+        const unsigned long long* wp = a.words + (RAW ? 0 : base);
+        const float* fp = a.raw + (RAW ? 3 * base : 0);
+        int jnext = 4 * h;  // first point of the next fetch
+        // operands of the next two stages are in flight while this one decodes
+        unsigned long long w1[4], w2[4];
+        float3 f1[4], f2[4];
+        auto fetch = [&](unsigned long long* w, float3* f) {
+            const int nv = live ? min(max(a.ns - jnext, 0), 4) : 0;
+            if (RAW) {
+                const float* p0 = fp;
+                const float* pq[4] = {p0, p0 + 3 * plane, p0 + 3 * plane2, p0 + 3 * plane3};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    f[q] = q < nv ? make_float3(__ldg(pq[q]), __ldg(pq[q] + 1), __ldg(pq[q] + 2))
+                                  : make_float3(0.f, 0.f, 0.f);
+                fp += 3 * step;
+            } else {
+                const unsigned long long* pq[4] = {wp, wp + plane, wp + plane2, wp + plane3};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) w[q] = q < nv ? __ldg(pq[q]) : 0ull;
+                wp += step;
+            }
+            jnext += kPts;
+        };
+        fetch(w1, f1);
+        fetch(w2, f2);
+        const int off = canon_off(row & (kHalf - 1), 4 * h);
+        int b = 0, use = 0;  // ring slot and how often it has been filled before
+        for (int s = 0; s < a.nst; ++s) {
+            unsigned long long w[4];
+            float3 f[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                w[q] = w1[q]; f[q] = f1[q];
+                w1[q] = w2[q]; f1[q] = f2[q];
+            }
+            fetch(w2, f2);  // beyond the last stage: no point valid, nothing loaded
+            float x[4], y[4], z[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (RAW) {
+                    x[q] = f[q].x; y[q] = f[q].y; z[q] = f[q].z;
+                } else {
+                    // zero words (and padding) decode to exact zeros
+                    decompress_one<TABLE, true>(w[q], P, tt, tp, x[q], y[q], z[q]);
+                }
+            }
+            if (use > 0) mbar_wait(&empty[b], (use - 1) & 1);
+            unsigned char* st = stages + (size_t)b * sbytes;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const float* v = d == 0 ? x : (d == 1 ? y : z);
+                float4 hi, lo;
+                hi.x = tf32_hi(v[0]); lo.x = v[0] - hi.x;
+                hi.y = tf32_hi(v[1]); lo.y = v[1] - hi.y;
+                hi.z = tf32_hi(v[2]); lo.z = v[2] - hi.z;
+                hi.w = tf32_hi(v[3]); lo.w = v[3] - hi.w;
+                *reinterpret_cast<float4*>(st + a_slice(0, m, d) + off) = hi;
+                *reinterpret_cast<float4*>(st + a_slice(1, m, d) + off) = lo;
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[b]);
+            if (++b == a.nbuf) { b = 0; ++use; }
+        }
+        // ---------------- epilogue: TMEM -> global ----------------
+        // warp -> TMEM lane quarter (warp % 4), accumulator half and column half
+        mbar_wait(accum_full, 0);
+        tc_fence_after();
+        const int quarter = warp & 3, part = warp >> 2;
+        const int em = part >> 1, chalf = part & 1;
+        const int64_t ei = i0 + em * kHalf + quarter * 32 + lane;
+        const int ncol = a.npad / 2;
+        const int64_t cstride = (int64_t)a.n_vars * a.ld;
+        float* op = a.out + ((int64_t)(chalf * ncol) * a.n_vars + c) * a.ld + ei;
+        const bool elive = ei < a.n_elem;
+        for (int c0 = chalf * ncol; c0 < (chalf + 1) * ncol; c0 += 16) {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(em * a.npad + c0), v);
+            const int kn = min(16, a.ns - c0);
+            if (elive) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    if (q < kn) op[0] = v[q];
+                    op += cstride;
+                }
+            } else {
+                op += 16 * cstride;
+            }
+        }
+    } else if (warp == kLoadWarp) {
+        // ---------------- operator slices (L2 -> smem, bulk async copy) ----------------
+        if (lane == 0) {
+            const uint32_t bbytes = 6 * b_slice_bytes(a.npad);
+            int b = 0, use = 0;
+            for (int s = 0; s < a.nst; ++s) {
+                if (use > 0) mbar_wait(&empty[b], (use - 1) & 1);
+                unsigned char* dst = stages + (size_t)b * sbytes + 12 * kASliceBytes;
+                mbar_arrive_tx(&full[b], bbytes);
+                bulk_g2s(dst, a.bprep + (size_t)s * (bbytes / 4), bbytes, &full[b]);
+                if (++b == a.nbuf) { b = 0; ++use; }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kMmaWarp) {
+        // ---------------- MMA issue (one thread) ----------------
+        if (lane == 0) {
+            const uint32_t idesc = idesc_tf32(kHalf, a.npad);
+            const int bsl = b_slice_bytes(a.npad);
+            int b = 0, use = 0;
+            for (int s = 0; s < a.nst; ++s) {
+                mbar_wait(&full[b], use & 1);
+                tc_fence_after();
+                const unsigned char* st = stages + (size_t)b * sbytes;
+                const unsigned char* bs = st + 12 * kASliceBytes;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const uint64_t bhi = smem_desc(bs + d * bsl, 128, 256);
+                    const uint64_t blo = smem_desc(bs + (3 + d) * bsl, 128, 256);
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+                        const uint32_t acc = tmem + (uint32_t)(m * a.npad);
+                        const uint64_t ahi = smem_desc(st + a_slice(0, m, d), 128, 256);
+                        const uint64_t alo = smem_desc(st + a_slice(1, m, d), 128, 256);
+                        mma_tf32(acc, alo, bhi, idesc, (s | d) != 0);
+                        mma_tf32(acc, ahi, blo, idesc, 1);
+                        mma_tf32(acc, ahi, bhi, idesc, 1);
+                    }
+                }
+                mma_commit(&empty[b]);
+                if (++b == a.nbuf) { b = 0; ++use; }
+            }
+            mma_commit(accum_full);
+        }
+        __syncwarp();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+    }
+}
+
+int npad_for(int ns) { return ((ns + 15) / 16) * 16; }
+int nst_for(int ns) { return (ns + kPts - 1) / kPts; }
+
+int fr_launch(const unsigned long long* words, const float* raw, const float* bprep, float* out,
+              int64_t n_elem, int n_vars, int64_t ld, int ns, const vc3_layout* layout, cudaStream_t s) {
+    if (n_elem < 0 || n_vars < 1 || ns < 1 || ns > 256 || ld < n_elem) return VC3_ERR_ARG;
+    if (!bprep || !out || (!words && !raw)) return VC3_ERR_ARG;
+    if (((uintptr_t)bprep & 15u) != 0) return VC3_ERR_ARG;
+    if (n_elem == 0) return VC3_OK;
+    FrArgs a{};
+    a.words = words;
+    a.raw = raw;
+    a.bprep = bprep;
+    a.out = out;
+    a.n_elem = n_elem;
+    a.ld = ld;
+    a.n_vars = n_vars;
+    a.ns = ns;
+    a.npad = npad_for(ns);
+    a.nst = nst_for(ns);
+    Params P{};
+    const double2* tab = nullptr;
+    size_t tab_bytes = 0;
+    if (!raw) {
+        if (!layout_ok(*layout)) return VC3_ERR_LAYOUT;
+        P = make_params(*layout);
+        const int st = get_table(P, &tab);
+        if (st) return st;
+        tab_bytes = table_smem(P);
+    }
+    const size_t sb = (size_t)stage_bytes(a.npad);
+    const size_t budget = 227 * 1024 - 1024 - tab_bytes;
+    int nbuf = (int)(budget / sb);
+    if (nbuf > 4) nbuf = 4;
+    if (nbuf > a.nst) nbuf = a.nst;
+    if (nbuf < 1) return VC3_ERR_ARG;
+    a.nbuf = nbuf;
+    const size_t smem = (size_t)nbuf * sb + 1024 + tab_bytes;
+    const int64_t tiles = ((n_elem + kRows - 1) / kRows) * n_vars;
+    if (tiles > 0x7fffffff) return VC3_ERR_ARG;
+    const void* fn;
+    if (raw) fn = (const void*)k_fr_div<true, false, RuntimeLayout>;
+    else if (is_default_layout(*layout)) fn = (const void*)k_fr_div<false, true, DefaultLayout>;
+    else if (P.table_mode) fn = (const void*)k_fr_div<false, true, RuntimeLayout>;
+    else fn = (const void*)k_fr_div<false, false, RuntimeLayout>;
+    int st = ensure_smem(fn, smem);
+    if (st) return st;
+    if (raw) k_fr_div<true, false, RuntimeLayout><<<(unsigned)tiles, kThreadsFr, smem, s>>>(a, P, tab);
+    else if (is_default_layout(*layout))
+        k_fr_div<false, true, DefaultLayout><<<(unsigned)tiles, kThreadsFr, smem, s>>>(a, P, tab);
+    else if (P.table_mode)
+        k_fr_div<false, true, RuntimeLayout><<<(unsigned)tiles, kThreadsFr, smem, s>>>(a, P, tab);
+    else
+        k_fr_div<false, false, RuntimeLayout><<<(unsigned)tiles, kThreadsFr, smem, s>>>(a, P, tab);
+    return launch_status();
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t vc3_fr_operator_floats(int n_points) {
+    if (n_points < 1 || n_points > 256) return -1;
+    return (int64_t)nst_for(n_points) * 6 * npad_for(n_points) * kPts;
+}
+
+int vc3_fr_prepare_operator(const float* D, int n_points, float* op, void* stream) {
+    if (!D || !op || n_points < 1 || n_points > 256) return VC3_ERR_ARG;
+    const int64_t total = vc3_fr_operator_floats(n_points);
+    const int grid = (int)((total + 255) / 256);
+    k_fr_prepare<<<grid, 256, 0, (cudaStream_t)stream>>>(D, n_points, npad_for(n_points),
+                                                          nst_for(n_points), op);
+    return launch_status();
+}
+
+int vc3_fr_divergence(const uint64_t* words, const float* op, float* div, int64_t n_elem,
+                      int n_vars, int64_t ld, int n_points, vc3_layout layout, void* stream) {
+    if (!words) return VC3_ERR_ARG;
+    return fr_launch((const unsigned long long*)words, nullptr, op, div, n_elem, n_vars, ld, n_points,
+                     &layout, (cudaStream_t)stream);
+}
+
+int vc3_fr_divergence_f32(const float* flux, const float* op, float* div, int64_t n_elem,
+                          int n_vars, int64_t ld, int n_points, void* stream) {
+    if (!flux) return VC3_ERR_ARG;
+    return fr_launch(nullptr, flux, op, div, n_elem, n_vars, ld, n_points, nullptr,
+                     (cudaStream_t)stream);
+}
+
+}  // extern "C"

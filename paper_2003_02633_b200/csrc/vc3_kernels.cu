@@ -19,6 +19,7 @@
 
 #include "../../include/vc3_b200.h"
 #include "vc3_device.cuh"
+#include "vc3_rt.h"
 
 using namespace vc3;
 
@@ -29,7 +30,9 @@ using namespace vc3;
 #endif
 constexpr bool kFma = VC3_USE_FMA != 0;
 
-namespace {
+// Host runtime shared with the other translation units (vc3_rt.h).
+namespace vc3 {
+namespace rt {
 
 thread_local int g_last_cuda = 0;
 
@@ -59,26 +62,6 @@ int sm_count() {
         count = 148;
     counts[dev] = count;
     return count;
-}
-
-constexpr int kThreads = 256;
-// measured on B200 (tools/occupancy_sweep.py): 4 vectors per thread step and
-// >= 4 resident CTAs per SM (<= 64 registers) give the best fused-add issue rate
-#ifndef VC3_FUSED_MIN_BLOCKS
-#define VC3_FUSED_MIN_BLOCKS 4
-#endif
-#ifndef VC3_DECOMP_STAGE
-#define VC3_DECOMP_STAGE 1
-#endif
-
-
-// grid for `items` work items of one thread each: at most `per_sm` CTAs per
-// SM (grid-stride beyond that), at least one.
-unsigned grid_for(int64_t items, int per_sm = 8) {
-    int64_t blocks = (items + kThreads - 1) / kThreads;
-    int64_t cap = (int64_t)sm_count() * per_sm;
-    if (blocks > cap) blocks = cap;
-    return (unsigned)(blocks < 1 ? 1 : blocks);
 }
 
 bool layout_ok(const vc3_layout& L) {
@@ -209,6 +192,32 @@ int ensure_smem(const void* func, size_t bytes) {
         cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     if (st == VC3_OK) done[key] = bytes;
     return st;
+}
+
+}  // namespace rt
+}  // namespace vc3
+using namespace vc3::rt;
+
+namespace {
+
+constexpr int kThreads = 256;
+// measured on B200 (tools/occupancy_sweep.py): 4 vectors per thread step and
+// >= 4 resident CTAs per SM (<= 64 registers) give the best fused-add issue rate
+#ifndef VC3_FUSED_MIN_BLOCKS
+#define VC3_FUSED_MIN_BLOCKS 4
+#endif
+#ifndef VC3_DECOMP_STAGE
+#define VC3_DECOMP_STAGE 1
+#endif
+
+
+// grid for `items` work items of one thread each: at most `per_sm` CTAs per
+// SM (grid-stride beyond that), at least one.
+unsigned grid_for(int64_t items, int per_sm = 8) {
+    int64_t blocks = (items + kThreads - 1) / kThreads;
+    int64_t cap = (int64_t)sm_count() * per_sm;
+    if (blocks > cap) blocks = cap;
+    return (unsigned)(blocks < 1 ? 1 : blocks);
 }
 
 // launch a table kernel: opt in to its shared-memory size first

@@ -1,0 +1,95 @@
+"""FR flux divergence (Alg. 1).
+
+CPU: the operator construction (exact on polynomials of degree <= k).
+GPU: the tcgen05 kernel against a float64 contraction of the decompressed
+fluxes (the oracle decodes the words bit-exactly), on the compressed and
+the float32 paths, ragged element counts, padded strides, ns = 8 .. 216.
+Tolerance: 3xTF32 products accumulate in fp32, so each output is checked
+to 2^-18 of sum_j,d |D| |X| (the fp32 sum itself carries ~ns * 2^-24)."""
+
+import numpy as np
+import pytest
+
+from conftest import layout_by_name, policy_by_code
+from paper_2003_02633_b200 import fr
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 5])
+def test_operator_exact_on_polynomials(k):
+    D = fr.divergence_operator(k, dtype=np.float64)
+    ns = (k + 1) ** 3
+    x, y, z = fr.solution_points(k).T
+    F = np.stack([x ** k * y, y ** (k - 1) * z + x, z ** k - y ** 2], axis=1)  # degree <= k per direction
+    div = np.einsum("djk,jd->k", D.reshape(3, ns, ns), F)
+    want = k * x ** (k - 1) * y + (k - 1) * y ** max(k - 2, 0) * z * (k > 1) + k * z ** (k - 1)
+    np.testing.assert_allclose(div, want, atol=1e-9 * ns)
+
+
+def _reference(D, X):
+    """float64 div[k][c][i] and the error scale sum |D||X|."""
+    ns = D.shape[1]
+    D3 = D.astype(np.float64).reshape(3, ns, ns)  # [d][j][k]
+    X = X.astype(np.float64)                      # [j][c][i][d]
+    ref = np.einsum("djk,jcid->kci", D3, X)
+    scale = np.einsum("djk,jcid->kci", np.abs(D3), np.abs(X))
+    return ref, scale
+
+
+def _check(got, ref, scale, what):
+    err = np.abs(got.astype(np.float64) - ref)
+    bound = 2.0 ** -18 * scale + 1e-30
+    worst = float((err / bound).max())
+    assert worst <= 1.0, f"{what}: worst error {worst:.3f} x bound"
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,n_elem,n_vars,pad", [(4, 1000, 5, 0), (4, 128, 1, 0), (1, 37, 2, 3),
+                                                  (2, 300, 3, 17), (5, 260, 2, 0), (4, 1, 5, 0)])
+def test_fr_divergence_matches_float64(oracle, vc3b, cuda, k, n_elem, n_vars, pad):
+    import torch
+
+    rng = np.random.default_rng(100 + k + n_elem)
+    ns = (k + 1) ** 3
+    ld = n_elem + pad
+    D = rng.standard_normal((3 * ns, ns)).astype(np.float32)
+    F = rng.uniform(-2, 2, (ns, n_vars, ld, 3)).astype(np.float32)
+    F[:, :, ::7] *= 1e-3          # mixed magnitudes
+    F[:, :, 5::11] = 0.0          # zero vectors
+    lay = vc3b.DEFAULT_LAYOUT
+    words = oracle.compress(F.reshape(-1, 3), lay, policy_by_code("SSS")).reshape(ns, n_vars, ld)
+    X = oracle.decompress(words.reshape(-1), lay).reshape(ns, n_vars, ld, 3)
+    op = fr.Operator(D)
+    got = fr.flux_divergence(torch.from_numpy(words.view(np.int64)).cuda().view(torch.uint64), op,
+                             n_elem).cpu().numpy()
+    ref, scale = _reference(D, X[:, :, :n_elem])
+    _check(got[:, :, :n_elem], ref, scale, f"compressed k={k}")
+    got32 = fr.flux_divergence_f32(torch.from_numpy(F).cuda(), op, n_elem).cpu().numpy()
+    ref32, scale32 = _reference(D, F[:, :, :n_elem])
+    _check(got32[:, :, :n_elem], ref32, scale32, f"f32 k={k}")
+
+
+@pytest.mark.gpu
+def test_fr_divergence_physical_operator_and_layouts(oracle, vc3b, cuda):
+    """The degree-4 hexahedron operator on a smooth field, two layouts
+    (table and wide-angle decode paths)."""
+    import torch
+
+    k, n_elem, n_vars = 4, 2000, 5
+    ns = 125
+    D = fr.divergence_operator(k)
+    xyz = fr.solution_points(k)
+    rng = np.random.default_rng(9)
+    a = rng.uniform(0.5, 1.5, (n_vars, n_elem))
+    F = np.empty((ns, n_vars, n_elem, 3), np.float32)
+    F[..., 0] = np.sin(xyz[:, 0])[:, None, None] * a
+    F[..., 1] = (xyz[:, 1] ** 2)[:, None, None] * a
+    F[..., 2] = np.cos(xyz[:, 2])[:, None, None] + 0 * a
+    op = fr.Operator(D)
+    for lname in ("17_18", "wide_10_25"):
+        lay = layout_by_name(lname)
+        words = oracle.compress(F.reshape(-1, 3), lay, policy_by_code("SSS")).reshape(ns, n_vars, n_elem)
+        X = oracle.decompress(words.reshape(-1), lay).reshape(ns, n_vars, n_elem, 3)
+        got = fr.flux_divergence(torch.from_numpy(words.view(np.int64)).cuda().view(torch.uint64),
+                                 op, layout=lay).cpu().numpy()
+        ref, scale = _reference(D, X)
+        _check(got, ref, scale, lname)
