@@ -44,9 +44,10 @@ constexpr int kRows = 256;             // elements per tile: two UMMA M = 128 ha
 constexpr int kHalf = 128;
 constexpr int kPts = 8;                // solution points per K stage
 constexpr int kDecodeWarps = 16;       // 2 threads per element, 4 points each
-constexpr int kThreadsFr = (kDecodeWarps + 2) * 32;
-constexpr int kLoadWarp = kDecodeWarps;
-constexpr int kMmaWarp = kDecodeWarps + 1;
+constexpr int kEpiWarps = 4;           // TMEM -> global, one per TMEM lane quarter
+constexpr int kThreadsFr = (kDecodeWarps + kEpiWarps + 2) * 32;
+constexpr int kLoadWarp = kDecodeWarps + kEpiWarps;
+constexpr int kMmaWarp = kDecodeWarps + kEpiWarps + 1;
 constexpr int kASliceBytes = kHalf * kPts * 4;  // one half, one dimension, hi or lo: 4 KB
 
 __host__ __device__ constexpr int b_slice_bytes(int npad) { return npad * kPts * 4; }
@@ -139,6 +140,46 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 
 __device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
+// fp32 decode for the contraction.  The GEMM rounds each product to ~2^-21
+// (3xTF32), so the operand needs no more than float32 accuracy: same table
+// index split as decompress_one<true> (vc3_device.cuh) with the table held
+// as float2 and the residual rotation psi <= 2 pi / 2^11 evaluated to
+// sin psi ~ psi - psi^3/6, cos psi - 1 ~ -psi^2/2 (truncation < 2^-40).
+// Agreement with vc3_decompress: a few float32 ulp (tests/test_fr.py).
+__device__ __forceinline__ void sincos_tab_f(const float2* __restrict__ tab, int idx, int lo,
+                                             float delta, float& s, float& c) {
+    const float2 A = tab[idx];
+    // lo < 2^23: exact int -> float on the FMA pipe
+    const float lof = __fsub_rn(__int_as_float(0x4B000000 | lo), 8388608.0f);
+    const float psi = __fmul_rn(lof, delta);
+    const float u = __fmul_rn(psi, psi);
+    const float sps = __fmaf_rn(__fmul_rn(psi, u), -0.16666667f, psi);
+    const float cm1 = __fmul_rn(u, -0.5f);
+    s = __fmaf_rn(A.y, sps, __fmaf_rn(A.x, cm1, A.x));
+    c = __fmaf_rn(-A.x, sps, __fmaf_rn(A.y, cm1, A.y));
+}
+
+template <class LAY>
+__device__ __forceinline__ void decode_f32(unsigned long long w, const Params& P, const float2* tab_t,
+                                           const float2* tab_p, float& ox, float& oy, float& oz) {
+    const unsigned long long field = w >> (P.p + P.t);
+    const int nt = (int)((unsigned)w & (unsigned)P.tmask);
+    const int nph = (int)((unsigned)(w >> P.t) & (unsigned)P.pmask);
+    const bool endp = nt == (int)P.ntmax;
+    const int it = endp ? P.t_n - 1 : (nt >> P.t_shift);
+    const int lt = endp ? 0 : (nt & ((1 << P.t_shift) - 1));
+    const bool pole = nph == (int)P.npmax;
+    const int ip = pole ? P.p_n - 1 : (nph >> P.p_shift);
+    const int lp = pole ? 0 : (nph & ((1 << P.p_shift) - 1));
+    float st, ct, sp, cp;
+    sincos_tab_f(tab_t, it, lt, (float)P.t_delta, st, ct);
+    sincos_tab_f(tab_p, ip, lp, (float)P.p_delta, sp, cp);
+    const float r = decode_mag(field, P);  // exact float32 magnitude, 0 for a zero field
+    ox = __fmul_rn(__fmul_rn(r, ct), sp);
+    oy = __fmul_rn(__fmul_rn(r, st), sp);
+    oz = __fmul_rn(r, cp);
+}
+
 // offset of (row, kk) inside one canonical K-major slice of 8 k-values:
 // core matrices of 8 rows x 16 B; LBO (next 4 k-values) = 128 B, SBO (next
 // 8 rows) = 256 B
@@ -186,21 +227,26 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
     unsigned char* stages = smem;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)a.nbuf * sbytes);
     uint64_t* empty = full + a.nbuf;
-    uint64_t* accum_full = empty + a.nbuf;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum_full + 1);
-    double2* s_tab = reinterpret_cast<double2*>(smem + (size_t)a.nbuf * sbytes + 1024);
-    const uint32_t tmem_cols = 2 * a.npad <= 256 ? 256 : 512;
+    uint64_t* acc_full = empty + a.nbuf;  // [2]
+    uint64_t* acc_empty = acc_full + 2;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    float2* s_tab = reinterpret_cast<float2*>(smem + (size_t)a.nbuf * sbytes + 1024);
+    // accumulators: [buffer][half] x npad fp32 columns; two buffers when they fit
+    const int nacc = 4 * a.npad <= 512 ? 2 : 1;
+    const uint32_t tmem_cols = nacc * 2 * a.npad <= 256 ? 256 : 512;
 
     const int64_t tiles_per_var = (a.n_elem + kRows - 1) / kRows;
-    const int c = (int)(blockIdx.x / tiles_per_var);
-    const int64_t i0 = (blockIdx.x - (int64_t)c * tiles_per_var) * kRows;
+    const int64_t ntiles = tiles_per_var * a.n_vars;
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < a.nbuf; ++b) {
             mbar_init(&full[b], kDecodeWarps + 1);
             mbar_init(&empty[b], 1);
         }
-        mbar_init(accum_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], kEpiWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -210,7 +256,10 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (!RAW && TABLE) {
-        for (int t = threadIdx.x; t < P.tab_n; t += blockDim.x) s_tab[t] = gtab[t];
+        for (int t = threadIdx.x; t < P.tab_n; t += blockDim.x) {
+            const double2 e = gtab[t];
+            s_tab[t] = make_float2((float)e.x, (float)e.y);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -218,27 +267,35 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
     const uint32_t tmem = *tmem_slot;
 
     if (warp < kDecodeWarps) {
-        // ---------------- producers of A (decode) ----------------
+        // ---------------- producers of A (decode), all tiles of this CTA ----------------
         const int row = threadIdx.x & (kRows - 1), h = threadIdx.x / kRows;
         const int m = row / kHalf;
-        const int64_t i = i0 + row;
-        const bool live = i < a.n_elem;
-        const double2* tt = s_tab;
-        const double2* tp = s_tab + P.p_base;
+        const float2* tt = s_tab;
+        const float2* tp = s_tab + P.p_base;
         const int64_t plane = (int64_t)a.n_vars * a.ld;  // stride between solution points
-        const int64_t base = (int64_t)c * a.ld + i + (int64_t)(4 * h) * plane;
         const int64_t plane2 = 2 * plane, plane3 = 3 * plane, step = (int64_t)kPts * plane;
-        const unsigned long long* wp = a.words + (RAW ? 0 : base);
-        const float* fp = a.raw + (RAW ? 3 * base : 0);
-        int jnext = 4 * h;  // first point of the next fetch
-        // operands of the next two stages are in flight while this one decodes
+        // fetch cursor: runs two stages ahead of the decode, across tile boundaries
+        int64_t ftile = blockIdx.x;
+        int fstage = 0;
+        const unsigned long long* wp = nullptr;
+        const float* fp = nullptr;
+        bool flive = false;
+        auto begin_tile = [&](int64_t t) {
+            const int c = (int)(t / tiles_per_var);
+            const int64_t i = (t - (int64_t)c * tiles_per_var) * kRows + row;
+            flive = t < ntiles && i < a.n_elem;
+            const int64_t base = (int64_t)c * a.ld + i + (int64_t)(4 * h) * plane;
+            wp = a.words + (RAW ? 0 : base);
+            fp = a.raw + (RAW ? 3 * base : 0);
+        };
+        begin_tile(ftile);
         unsigned long long w1[4], w2[4];
         float3 f1[4], f2[4];
         auto fetch = [&](unsigned long long* w, float3* f) {
-            const int nv = live ? min(max(a.ns - jnext, 0), 4) : 0;
+            const int jn = fstage * kPts + 4 * h;
+            const int nv = flive ? min(max(a.ns - jn, 0), 4) : 0;
             if (RAW) {
-                const float* p0 = fp;
-                const float* pq[4] = {p0, p0 + 3 * plane, p0 + 3 * plane2, p0 + 3 * plane3};
+                const float* pq[4] = {fp, fp + 3 * plane, fp + 3 * plane2, fp + 3 * plane3};
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     f[q] = q < nv ? make_float3(__ldg(pq[q]), __ldg(pq[q] + 1), __ldg(pq[q] + 2))
@@ -250,85 +307,107 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
                 for (int q = 0; q < 4; ++q) w[q] = q < nv ? __ldg(pq[q]) : 0ull;
                 wp += step;
             }
-            jnext += kPts;
+            if (++fstage == a.nst) {
+                fstage = 0;
+                ftile += gridDim.x;
+                begin_tile(ftile);
+            }
         };
         fetch(w1, f1);
         fetch(w2, f2);
         const int off = canon_off(row & (kHalf - 1), 4 * h);
         int b = 0, use = 0;  // ring slot and how often it has been filled before
-        for (int s = 0; s < a.nst; ++s) {
-            unsigned long long w[4];
-            float3 f[4];
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int s = 0; s < a.nst; ++s) {
+                unsigned long long w[4];
+                float3 f[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                w[q] = w1[q]; f[q] = f1[q];
-                w1[q] = w2[q]; f1[q] = f2[q];
-            }
-            fetch(w2, f2);  // beyond the last stage: no point valid, nothing loaded
-            float x[4], y[4], z[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (RAW) {
-                    x[q] = f[q].x; y[q] = f[q].y; z[q] = f[q].z;
-                } else {
-                    // zero words (and padding) decode to exact zeros
-                    decompress_one<TABLE, true>(w[q], P, tt, tp, x[q], y[q], z[q]);
+                for (int q = 0; q < 4; ++q) {
+                    w[q] = w1[q]; f[q] = f1[q];
+                    w1[q] = w2[q]; f1[q] = f2[q];
                 }
-            }
-            if (use > 0) mbar_wait(&empty[b], (use - 1) & 1);
-            unsigned char* st = stages + (size_t)b * sbytes;
+                fetch(w2, f2);
+                float x[4], y[4], z[4];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const float* v = d == 0 ? x : (d == 1 ? y : z);
-                float4 hi, lo;
-                hi.x = tf32_hi(v[0]); lo.x = v[0] - hi.x;
-                hi.y = tf32_hi(v[1]); lo.y = v[1] - hi.y;
-                hi.z = tf32_hi(v[2]); lo.z = v[2] - hi.z;
-                hi.w = tf32_hi(v[3]); lo.w = v[3] - hi.w;
-                *reinterpret_cast<float4*>(st + a_slice(0, m, d) + off) = hi;
-                *reinterpret_cast<float4*>(st + a_slice(1, m, d) + off) = lo;
+                for (int q = 0; q < 4; ++q) {
+                    if (RAW) {
+                        x[q] = f[q].x; y[q] = f[q].y; z[q] = f[q].z;
+                    } else if (TABLE) {
+                        // zero words (and padding) decode to exact zeros
+                        decode_f32<LAY>(w[q], P, tt, tp, x[q], y[q], z[q]);
+                    } else {
+                        decompress_one<false, true>(w[q], P, nullptr, nullptr, x[q], y[q], z[q]);
+                    }
+                }
+                if (use > 0) mbar_wait(&empty[b], (use - 1) & 1);
+                unsigned char* st = stages + (size_t)b * sbytes;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const float* v = d == 0 ? x : (d == 1 ? y : z);
+                    float4 hi, lo;
+                    hi.x = tf32_hi(v[0]); lo.x = v[0] - hi.x;
+                    hi.y = tf32_hi(v[1]); lo.y = v[1] - hi.y;
+                    hi.z = tf32_hi(v[2]); lo.z = v[2] - hi.z;
+                    hi.w = tf32_hi(v[3]); lo.w = v[3] - hi.w;
+                    *reinterpret_cast<float4*>(st + a_slice(0, m, d) + off) = hi;
+                    *reinterpret_cast<float4*>(st + a_slice(1, m, d) + off) = lo;
+                }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[b]);
+                if (++b == a.nbuf) { b = 0; ++use; }
             }
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[b]);
-            if (++b == a.nbuf) { b = 0; ++use; }
         }
-        // ---------------- epilogue: TMEM -> global ----------------
-        // warp -> TMEM lane quarter (warp % 4), accumulator half and column half
-        mbar_wait(accum_full, 0);
-        tc_fence_after();
-        const int quarter = warp & 3, part = warp >> 2;
-        const int em = part >> 1, chalf = part & 1;
-        const int64_t ei = i0 + em * kHalf + quarter * 32 + lane;
-        const int ncol = a.npad / 2;
+    } else if (warp < kDecodeWarps + kEpiWarps) {
+        // ---------------- epilogue: TMEM -> global, overlapping the next tile ----------------
+        const int ew = warp - kDecodeWarps;  // == warp % 4: TMEM lane quarter
         const int64_t cstride = (int64_t)a.n_vars * a.ld;
-        float* op = a.out + ((int64_t)(chalf * ncol) * a.n_vars + c) * a.ld + ei;
-        const bool elive = ei < a.n_elem;
-        for (int c0 = chalf * ncol; c0 < (chalf + 1) * ncol; c0 += 16) {
-            float v[16];
-            tmem_ld16(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(em * a.npad + c0), v);
-            const int kn = min(16, a.ns - c0);
-            if (elive) {
+        int lt = 0;
+        for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+            const int ab = nacc == 2 ? (lt & 1) : 0;
+            const int au = nacc == 2 ? (lt >> 1) : lt;
+            mbar_wait(&acc_full[ab], au & 1);
+            tc_fence_after();
+            const int c = (int)(t / tiles_per_var);
+            const int64_t i0 = (t - (int64_t)c * tiles_per_var) * kRows;
+#pragma unroll 1
+            for (int em = 0; em < 2; ++em) {
+                const int64_t ei = i0 + em * kHalf + ew * 32 + lane;
+                const bool elive = ei < a.n_elem;
+                float* op = a.out + (int64_t)c * a.ld + ei;
+                const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)((ab * 2 + em) * a.npad);
+                for (int c0 = 0; c0 < a.npad; c0 += 16) {
+                    float v[16];
+                    tmem_ld16(tbase + (uint32_t)c0, v);
+                    const int kn = min(16, a.ns - c0);
+                    if (elive) {
 #pragma unroll
-                for (int q = 0; q < 16; ++q) {
-                    if (q < kn) op[0] = v[q];
-                    op += cstride;
+                        for (int q = 0; q < 16; ++q) {
+                            if (q < kn) op[0] = v[q];
+                            op += cstride;
+                        }
+                    } else {
+                        op += 16 * cstride;
+                    }
                 }
-            } else {
-                op += 16 * cstride;
             }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
         }
     } else if (warp == kLoadWarp) {
         // ---------------- operator slices (L2 -> smem, bulk async copy) ----------------
         if (lane == 0) {
             const uint32_t bbytes = 6 * b_slice_bytes(a.npad);
             int b = 0, use = 0;
-            for (int s = 0; s < a.nst; ++s) {
-                if (use > 0) mbar_wait(&empty[b], (use - 1) & 1);
-                unsigned char* dst = stages + (size_t)b * sbytes + 12 * kASliceBytes;
-                mbar_arrive_tx(&full[b], bbytes);
-                bulk_g2s(dst, a.bprep + (size_t)s * (bbytes / 4), bbytes, &full[b]);
-                if (++b == a.nbuf) { b = 0; ++use; }
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                for (int s = 0; s < a.nst; ++s) {
+                    if (use > 0) mbar_wait(&empty[b], (use - 1) & 1);
+                    unsigned char* dst = stages + (size_t)b * sbytes + 12 * kASliceBytes;
+                    mbar_arrive_tx(&full[b], bbytes);
+                    bulk_g2s(dst, a.bprep + (size_t)s * (bbytes / 4), bbytes, &full[b]);
+                    if (++b == a.nbuf) { b = 0; ++use; }
+                }
             }
         }
         __syncwarp();
@@ -337,30 +416,36 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
         if (lane == 0) {
             const uint32_t idesc = idesc_tf32(kHalf, a.npad);
             const int bsl = b_slice_bytes(a.npad);
-            int b = 0, use = 0;
-            for (int s = 0; s < a.nst; ++s) {
-                mbar_wait(&full[b], use & 1);
+            int b = 0, use = 0, lt = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
+                const int ab = nacc == 2 ? (lt & 1) : 0;
+                const int au = nacc == 2 ? (lt >> 1) : lt;
+                if (au > 0) mbar_wait(&acc_empty[ab], (au - 1) & 1);  // epilogue drained it
                 tc_fence_after();
-                const unsigned char* st = stages + (size_t)b * sbytes;
-                const unsigned char* bs = st + 12 * kASliceBytes;
+                for (int s = 0; s < a.nst; ++s) {
+                    mbar_wait(&full[b], use & 1);
+                    tc_fence_after();
+                    const unsigned char* st = stages + (size_t)b * sbytes;
+                    const unsigned char* bs = st + 12 * kASliceBytes;
 #pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const uint64_t bhi = smem_desc(bs + d * bsl, 128, 256);
-                    const uint64_t blo = smem_desc(bs + (3 + d) * bsl, 128, 256);
+                    for (int d = 0; d < 3; ++d) {
+                        const uint64_t bhi = smem_desc(bs + d * bsl, 128, 256);
+                        const uint64_t blo = smem_desc(bs + (3 + d) * bsl, 128, 256);
 #pragma unroll
-                    for (int m = 0; m < 2; ++m) {
-                        const uint32_t acc = tmem + (uint32_t)(m * a.npad);
-                        const uint64_t ahi = smem_desc(st + a_slice(0, m, d), 128, 256);
-                        const uint64_t alo = smem_desc(st + a_slice(1, m, d), 128, 256);
-                        mma_tf32(acc, alo, bhi, idesc, (s | d) != 0);
-                        mma_tf32(acc, ahi, blo, idesc, 1);
-                        mma_tf32(acc, ahi, bhi, idesc, 1);
+                        for (int m = 0; m < 2; ++m) {
+                            const uint32_t acc = tmem + (uint32_t)((ab * 2 + m) * a.npad);
+                            const uint64_t ahi = smem_desc(st + a_slice(0, m, d), 128, 256);
+                            const uint64_t alo = smem_desc(st + a_slice(1, m, d), 128, 256);
+                            mma_tf32(acc, alo, bhi, idesc, (s | d) != 0);
+                            mma_tf32(acc, ahi, blo, idesc, 1);
+                            mma_tf32(acc, ahi, bhi, idesc, 1);
+                        }
                     }
+                    mma_commit(&empty[b]);
+                    if (++b == a.nbuf) { b = 0; ++use; }
                 }
-                mma_commit(&empty[b]);
-                if (++b == a.nbuf) { b = 0; ++use; }
+                mma_commit(&acc_full[ab]);
             }
-            mma_commit(accum_full);
         }
         __syncwarp();
     }
@@ -400,7 +485,7 @@ int fr_launch(const unsigned long long* words, const float* raw, const float* bp
         P = make_params(*layout);
         const int st = get_table(P, &tab);
         if (st) return st;
-        tab_bytes = table_smem(P);
+        tab_bytes = table_smem(P) / 2;  // held as float2
     }
     const size_t sb = (size_t)stage_bytes(a.npad);
     const size_t budget = 227 * 1024 - 1024 - tab_bytes;
@@ -411,7 +496,7 @@ int fr_launch(const unsigned long long* words, const float* raw, const float* bp
     a.nbuf = nbuf;
     const size_t smem = (size_t)nbuf * sb + 1024 + tab_bytes;
     const int64_t tiles = ((n_elem + kRows - 1) / kRows) * n_vars;
-    if (tiles > 0x7fffffff) return VC3_ERR_ARG;
+    const int64_t grid = tiles < sm_count() ? tiles : sm_count();  // persistent: one CTA per SM
     const void* fn;
     if (raw) fn = (const void*)k_fr_div<true, false, RuntimeLayout>;
     else if (is_default_layout(*layout)) fn = (const void*)k_fr_div<false, true, DefaultLayout>;
@@ -419,13 +504,13 @@ int fr_launch(const unsigned long long* words, const float* raw, const float* bp
     else fn = (const void*)k_fr_div<false, false, RuntimeLayout>;
     int st = ensure_smem(fn, smem);
     if (st) return st;
-    if (raw) k_fr_div<true, false, RuntimeLayout><<<(unsigned)tiles, kThreadsFr, smem, s>>>(a, P, tab);
+    if (raw) k_fr_div<true, false, RuntimeLayout><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P, tab);
     else if (is_default_layout(*layout))
-        k_fr_div<false, true, DefaultLayout><<<(unsigned)tiles, kThreadsFr, smem, s>>>(a, P, tab);
+        k_fr_div<false, true, DefaultLayout><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P, tab);
     else if (P.table_mode)
-        k_fr_div<false, true, RuntimeLayout><<<(unsigned)tiles, kThreadsFr, smem, s>>>(a, P, tab);
+        k_fr_div<false, true, RuntimeLayout><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P, tab);
     else
-        k_fr_div<false, false, RuntimeLayout><<<(unsigned)tiles, kThreadsFr, smem, s>>>(a, P, tab);
+        k_fr_div<false, false, RuntimeLayout><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P, tab);
     return launch_status();
 }
 
