@@ -70,6 +70,14 @@ def measured_peak() -> tuple[float, str]:
     return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return json.loads(p.read_text()) if p.exists() else {}
+    except ValueError:
+        return {}
+
+
 def ncu_traffic() -> float | None:
     """DRAM bytes per fused-add launch from the committed ncu capture."""
     p = ROOT / "profiles" / "ncu_add_traffic.json"
@@ -309,6 +317,46 @@ def run_secondary(args, vc3b, lib, dev, stream, n):
         "fp32_hbm_gb_s": 60 * npts / (tf * 1e-3) / 1e9,
         "speedup_vs_fp32": tf / tc}
     del q, dq, R, qf, dqf, Rf, vel
+    torch.cuda.empty_cache()
+
+    # C6: FR flux divergence (Alg. 1) on the tcgen05 kernel,
+    # degree-4 hexahedra, 5 equation rows per point, compressed vs float32 fluxes
+    from paper_2003_02633_b200 import fr
+
+    kdeg, n_vars, n_el = 4, 5, 1 << 18
+    ns = (kdeg + 1) ** 3
+    op = fr.Operator(fr.divergence_operator(kdeg))
+    mom, vel = fields.icv_fields(n_el, 30.0, device=dev)
+    F = torch.stack([mom.reshape(ns, n_el, 3) * (1.0 + 0.25 * c_) for c_ in range(n_vars - 1)]
+                    + [vel.reshape(ns, n_el, 3)], dim=1).contiguous()
+    del mom, vel
+    words = vc3b.compress(F.reshape(-1, 3), lay, vc3b.ALL_SINGLE_POLICY).reshape(ns, n_vars, n_el)
+    div = torch.empty((ns, n_vars, n_el), dtype=torch.float32, device=dev)
+    fc = lambda: lib.vc3_fr_divergence(words.data_ptr(), op.staged.data_ptr(), div.data_ptr(), n_el,
+                                       n_vars, n_el, ns, cl, stream.cuda_stream)
+    ff = lambda: lib.vc3_fr_divergence_f32(F.data_ptr(), op.staged.data_ptr(), div.data_ptr(), n_el,
+                                           n_vars, n_el, ns, stream.cuda_stream)
+    fc(); ff()
+    torch.cuda.synchronize()
+    tcm = time_region(fc, steps, stream, torch)
+    tf3 = time_region(ff, steps, stream, torch)
+    rows = n_el * n_vars
+    dense = 2.0 * 3 * ns * ns * rows  # flops of Alg. 1 per launch
+    tf32_peak = load_peaks().get("bf16_tflops", 2250.0) / 2.0
+    ach = 3 * dense / (tcm * 1e-3) / 1e12
+    out["C6_fr_divergence"] = {
+        "k": kdeg, "n_points": ns, "n_vars": n_vars, "n_elem": n_el, "unit": "G elem-eq/s",
+        "field": "ICV momentum/velocity rows, [ns][n_vars][n_elem] words",
+        "compressed": rows / (tcm * 1e-3) / 1e9, "fp32": rows / (tf3 * 1e-3) / 1e9,
+        "speedup_vs_fp32": tf3 / tcm,
+        "compressed_hbm_gb_s": rows * ns * 12 / (tcm * 1e-3) / 1e9,
+        "fp32_hbm_gb_s": rows * ns * 16 / (tf3 * 1e-3) / 1e9,
+        "dense_tflops": dense / (tcm * 1e-3) / 1e12,
+        "roofline": {"bound": "tensor", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
+                     "frac": ach / tf32_peak,
+                     "note": "3xTF32: 3 tensor products per Alg.-1 product; peak = half the "
+                             "measured dense bf16 rate (MEASURED_PEAKS.json)"}}
+    del F, words, div, op
     torch.cuda.empty_cache()
     return out
 
