@@ -336,10 +336,18 @@ def run_secondary(args, vc3b, lib, dev, stream, n):
                                        n_vars, n_el, ns, cl, stream.cuda_stream)
     ff = lambda: lib.vc3_fr_divergence_f32(F.data_ptr(), op.staged.data_ptr(), div.data_ptr(), n_el,
                                            n_vars, n_el, ns, stream.cuda_stream)
-    fc(); ff()
+    m1 = np.ascontiguousarray(fr.lagrange_derivative_matrix(fr.gauss_legendre_nodes(kdeg)),
+                              dtype=np.float32)
+    hc = lambda: lib.vc3_fr_divergence_hex(words.data_ptr(), m1.ctypes.data, kdeg, div.data_ptr(),
+                                           n_el, n_vars, n_el, cl, stream.cuda_stream)
+    hf = lambda: lib.vc3_fr_divergence_hex_f32(F.data_ptr(), m1.ctypes.data, kdeg, div.data_ptr(),
+                                               n_el, n_vars, n_el, stream.cuda_stream)
+    fc(); ff(); hc(); hf()
     torch.cuda.synchronize()
     tcm = time_region(fc, steps, stream, torch)
     tf3 = time_region(ff, steps, stream, torch)
+    thc = time_region(hc, steps, stream, torch)
+    thf = time_region(hf, steps, stream, torch)
     rows = n_el * n_vars
     dense = 2.0 * 3 * ns * ns * rows  # flops of Alg. 1 per launch
     tf32_peak = load_peaks().get("bf16_tflops", 2250.0) / 2.0
@@ -352,6 +360,10 @@ def run_secondary(args, vc3b, lib, dev, stream, n):
         "compressed_hbm_gb_s": rows * ns * 12 / (tcm * 1e-3) / 1e9,
         "fp32_hbm_gb_s": rows * ns * 16 / (tf3 * 1e-3) / 1e9,
         "dense_tflops": dense / (tcm * 1e-3) / 1e12,
+        "sum_factorised": {"compressed": rows / (thc * 1e-3) / 1e9, "fp32": rows / (thf * 1e-3) / 1e9,
+                           "compressed_hbm_gb_s": rows * ns * 12 / (thc * 1e-3) / 1e9,
+                           "fp32_hbm_gb_s": rows * ns * 16 / (thf * 1e-3) / 1e9,
+                           "note": "tensor-product hexahedron, 15 FMAs per output on CUDA cores"},
         "roofline": {"bound": "tensor", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
                      "frac": ach / tf32_peak,
                      "note": "3xTF32: 3 tensor products per Alg.-1 product; peak = half the "

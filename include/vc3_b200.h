@@ -190,6 +190,16 @@ int vc3_fr_divergence(const uint64_t* words, const float* op, float* div, int64_
 int vc3_fr_divergence_f32(const float* flux, const float* op, float* div, int64_t n_elem,
                           int n_vars, int64_t ld, int n_points, void* stream);
 
+/* Tensor-product hexahedra of degree 1..4 (n_points = (degree+1)^3, point
+ * index px + n py + n^2 pz): the same divergence with D built from the 1D
+ * derivative matrix m1d[a*(degree+1) + m] = l_m'(x_a) (HOST memory, read at
+ * launch), sum-factorised on the CUDA cores (3(degree+1) multiply-adds per
+ * output).  Table layouts only (angle fields <= 20 bits). */
+int vc3_fr_divergence_hex(const uint64_t* words, const float* m1d, int degree, float* div,
+                          int64_t n_elem, int n_vars, int64_t ld, vc3_layout layout, void* stream);
+int vc3_fr_divergence_hex_f32(const float* flux, const float* m1d, int degree, float* div,
+                              int64_t n_elem, int n_vars, int64_t ld, void* stream);
+
 /* ---- host-buffer entry points (reference-facing, synchronous) ------------
  * Same operations on HOST arrays: the call streams chunks host->device, runs
  * the kernel and copies results back, overlapping copies and compute on

@@ -68,6 +68,8 @@ SIGNATURES = {
     "vc3_fr_prepare_operator": ([_p, ctypes.c_int, _p, _p], ctypes.c_int),
     "vc3_fr_divergence": ([_p, _p, _p, _i64, ctypes.c_int, _i64, ctypes.c_int, Layout, _p], ctypes.c_int),
     "vc3_fr_divergence_f32": ([_p, _p, _p, _i64, ctypes.c_int, _i64, ctypes.c_int, _p], ctypes.c_int),
+    "vc3_fr_divergence_hex": ([_p, _p, ctypes.c_int, _p, _i64, ctypes.c_int, _i64, Layout, _p], ctypes.c_int),
+    "vc3_fr_divergence_hex_f32": ([_p, _p, ctypes.c_int, _p, _i64, ctypes.c_int, _i64, _p], ctypes.c_int),
     "vc3_add_compressed_host": ([_p, _p, _p, _i64, Layout, _u32, _i32], ctypes.c_int),
     "vc3_compress_host": ([_p, _p, _i64, Layout, _u32, _p, _i32], ctypes.c_int),
     "vc3_decompress_host": ([_p, _p, _i64, Layout, _i32], ctypes.c_int),

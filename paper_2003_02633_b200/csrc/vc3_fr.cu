@@ -514,6 +514,246 @@ int fr_launch(const unsigned long long* words, const float* raw, const float* bp
     return launch_status();
 }
 
+// ---- sum-factorised divergence for tensor-product hexahedra ---------------------
+// For D built from a 1D derivative matrix M (M[a][m] = l_m'(x_a), k+1 Gauss
+// points per direction, point index p = px + n py + n^2 pz), Alg. 1 reduces to
+//   div[k] = sum_a M[kx][a] X_(a,ky,kz).x + M[ky][a] X_(kx,a,kz).y
+//                                        + M[kz][a] X_(kx,ky,a).z,
+// 3(k+1) multiply-adds per output instead of 3 ns.  One thread per
+// (element, equation) streams its ns words in point order, decodes each once
+// and scatters its three components into the ns accumulators held in
+// registers (indices are compile-time: the point loop is fully unrolled).
+// No shared-memory staging and no tensor cores: the kernel is bound by HBM
+// and the decode, which is where the paper's compression argument applies.
+struct HexOp {
+    float m[6][6];
+};
+
+template <int K, bool RAW, class LAY>
+__global__ void __launch_bounds__(128) k_fr_hex(const unsigned long long* __restrict__ words,
+                                                const float* __restrict__ raw, float* __restrict__ out,
+                                                int64_t n_elem, int n_vars, int64_t ld, HexOp op,
+                                                Params Pin, const double2* __restrict__ gtab) {
+    constexpr int N1 = K + 1, NS = N1 * N1 * N1, PF = 8;
+    Params P = Pin;
+    LAY::apply(P);
+    extern __shared__ float2 s_tabf[];
+    if (!RAW) {
+        for (int t = threadIdx.x; t < P.tab_n; t += blockDim.x) {
+            const double2 e = gtab[t];
+            s_tabf[t] = make_float2((float)e.x, (float)e.y);
+        }
+        __syncthreads();
+    }
+    const float2* tt = s_tabf;
+    const float2* tp = s_tabf + P.p_base;
+    const int c = blockIdx.y;
+    const int64_t plane = (int64_t)n_vars * ld;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_elem;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t base = (int64_t)c * ld + i;
+        float acc[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) acc[k] = 0.0f;
+        unsigned long long pw[PF];
+        float3 pf[PF];
+#pragma unroll
+        for (int q = 0; q < PF; ++q) {
+            if (RAW) {
+                const float* p = raw + 3 * (base + q * plane);
+                pf[q] = make_float3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
+            } else {
+                pw[q] = __ldg(words + base + q * plane);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+            float x, y, z;
+            if (RAW) {
+                x = pf[j % PF].x; y = pf[j % PF].y; z = pf[j % PF].z;
+            } else {
+                decode_f32<LAY>(pw[j % PF], P, tt, tp, x, y, z);
+            }
+            if (j + PF < NS) {
+                if (RAW) {
+                    const float* p = raw + 3 * (base + (j + PF) * plane);
+                    pf[j % PF] = make_float3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
+                } else {
+                    pw[j % PF] = __ldg(words + base + (j + PF) * plane);
+                }
+            }
+            const int jx = j % N1, jy = (j / N1) % N1, jz = j / (N1 * N1);
+#pragma unroll
+            for (int a = 0; a < N1; ++a) {
+                acc[a + N1 * jy + N1 * N1 * jz] = __fmaf_rn(op.m[a][jx], x, acc[a + N1 * jy + N1 * N1 * jz]);
+                acc[jx + N1 * a + N1 * N1 * jz] = __fmaf_rn(op.m[a][jy], y, acc[jx + N1 * a + N1 * N1 * jz]);
+                acc[jx + N1 * jy + N1 * N1 * a] = __fmaf_rn(op.m[a][jz], z, acc[jx + N1 * jy + N1 * N1 * a]);
+            }
+        }
+        float* o = out + base;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) o[k * plane] = acc[k];
+    }
+}
+
+// Compressed fluxes: the per-thread decode above is latency-bound (all ns
+// accumulators live in registers, 2 warps per scheduler).  Here a CTA takes
+// 32 elements of one equation: phase A decodes the tile's 32 x ns words with
+// all 8 warps (loads issued up front, lane = element) into shared memory as
+// [dimension][point][element] floats; phase B applies the sum-factorised
+// operator from shared memory (15 conflict-free loads + 15 FMAs per output at
+// k = 4), lane = element, so global loads and stores stay 256/128-byte
+// coalesced rows.
+constexpr int kHexE = 32;
+constexpr int kHexThreads = 256;
+
+template <int K, class LAY>
+__global__ void __launch_bounds__(kHexThreads, 3) k_fr_hex_staged(
+    const unsigned long long* __restrict__ words, float* __restrict__ out, int64_t n_elem, int n_vars,
+    int64_t ld, HexOp op, Params Pin, const double2* __restrict__ gtab) {
+    constexpr int N1 = K + 1, NS = N1 * N1 * N1, NW = kHexThreads / 32;
+    constexpr int NJ = (NS + NW - 1) / NW;  // points per warp in phase A
+    Params P = Pin;
+    LAY::apply(P);
+    extern __shared__ float2 s_tabf[];
+    float* xs = reinterpret_cast<float*>(s_tabf + P.tab_n);  // [3][NS][kHexE]
+    for (int t = threadIdx.x; t < P.tab_n; t += blockDim.x) {
+        const double2 e = gtab[t];
+        s_tabf[t] = make_float2((float)e.x, (float)e.y);
+    }
+    __syncthreads();
+    const float2* tt = s_tabf;
+    const float2* tp = s_tabf + P.p_base;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t blocks_per_var = (n_elem + kHexE - 1) / kHexE;
+    const int64_t ntiles = blocks_per_var * n_vars;
+    const int64_t plane = (int64_t)n_vars * ld;
+    // the next tile's words are loaded while this tile runs phase B
+    unsigned long long w[NJ];
+    auto load_tile = [&](int64_t t) {
+        const int c = (int)(t / blocks_per_var);
+        const int64_t i = (t - (int64_t)c * blocks_per_var) * kHexE + lane;
+        const bool ok = t < ntiles && i < n_elem;
+        const unsigned long long* wp = words + (int64_t)c * ld + i;
+#pragma unroll
+        for (int r = 0; r < NJ; ++r) {
+            const int j = warp + NW * r;
+            w[r] = (ok && j < NS) ? __ldg(wp + j * plane) : 0ull;
+        }
+    };
+    load_tile(blockIdx.x);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int c = (int)(t / blocks_per_var);
+        const int64_t i = (t - (int64_t)c * blocks_per_var) * kHexE + lane;
+        const bool live = i < n_elem;
+        // phase A: decode
+#pragma unroll
+        for (int r = 0; r < NJ; ++r) {
+            const int j = warp + NW * r;
+            if (j < NS) {
+                float x, y, z;
+                decode_f32<LAY>(w[r], P, tt, tp, x, y, z);
+                xs[(0 * NS + j) * kHexE + lane] = x;
+                xs[(1 * NS + j) * kHexE + lane] = y;
+                xs[(2 * NS + j) * kHexE + lane] = z;
+            }
+        }
+        load_tile(t + gridDim.x);
+        __syncthreads();
+        // phase B: sum-factorised operator; a thread computes one x-line
+        // (ky, kz) of its element: the x-part reuses the line's N1 values,
+        // the 1D matrix rows of ky and kz are loaded once per line
+        float* op_out = out + (int64_t)c * ld + i;
+        for (int L = warp; L < N1 * N1; L += NW) {
+            const int ky = L % N1, kz = L / N1;
+            float my[N1], mz[N1], xv[N1], acc[N1];
+#pragma unroll
+            for (int a = 0; a < N1; ++a) {
+                my[a] = op.m[ky][a];
+                mz[a] = op.m[kz][a];
+                xv[a] = xs[(0 * NS + a + N1 * L) * kHexE + lane];
+            }
+#pragma unroll
+            for (int kx = 0; kx < N1; ++kx) {
+                float t = 0.0f;
+#pragma unroll
+                for (int a = 0; a < N1; ++a) t = __fmaf_rn(op.m[kx][a], xv[a], t);
+#pragma unroll
+                for (int a = 0; a < N1; ++a)
+                    t = __fmaf_rn(my[a], xs[(1 * NS + kx + N1 * a + N1 * N1 * kz) * kHexE + lane], t);
+#pragma unroll
+                for (int a = 0; a < N1; ++a)
+                    t = __fmaf_rn(mz[a], xs[(2 * NS + kx + N1 * ky + N1 * N1 * a) * kHexE + lane], t);
+                acc[kx] = t;
+            }
+            if (live) {
+#pragma unroll
+                for (int kx = 0; kx < N1; ++kx) op_out[(kx + N1 * L) * plane] = acc[kx];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int K>
+int hex_launch_k(const unsigned long long* words, const float* raw, float* out, int64_t n_elem,
+                 int n_vars, int64_t ld, const HexOp& op, const vc3_layout* layout, cudaStream_t s) {
+    Params P{};
+    const double2* tab = nullptr;
+    size_t smem = 0;
+    if (!raw) {
+        P = make_params(*layout);
+        if (!P.table_mode) return VC3_ERR_LAYOUT;  // wide layouts: use vc3_fr_divergence
+        const int st = get_table(P, &tab);
+        if (st) return st;
+        smem = table_smem(P) / 2;
+    }
+    int64_t blocks = (n_elem + 127) / 128;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (blocks > cap) blocks = cap;
+    const dim3 grid((unsigned)blocks, (unsigned)n_vars);
+    if (raw) {
+        k_fr_hex<K, true, RuntimeLayout><<<grid, 128, 0, s>>>(nullptr, raw, out, n_elem, n_vars, ld, op, P, tab);
+    } else {
+        constexpr int NS = (K + 1) * (K + 1) * (K + 1);
+        smem += (size_t)3 * NS * kHexE * sizeof(float);
+        const int64_t tiles = ((n_elem + kHexE - 1) / kHexE) * n_vars;
+        const int64_t cap3 = (int64_t)sm_count() * 3;  // three 73-KB CTAs per SM at k = 4
+        const unsigned g = (unsigned)(tiles < cap3 ? tiles : cap3);
+        if (is_default_layout(*layout)) {
+            const int st = ensure_smem((const void*)k_fr_hex_staged<K, DefaultLayout>, smem);
+            if (st) return st;
+            cudaFuncSetAttribute((const void*)k_fr_hex_staged<K, DefaultLayout>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+            k_fr_hex_staged<K, DefaultLayout><<<g, kHexThreads, smem, s>>>(words, out, n_elem, n_vars, ld, op, P, tab);
+        } else {
+            const int st = ensure_smem((const void*)k_fr_hex_staged<K, RuntimeLayout>, smem);
+            if (st) return st;
+            k_fr_hex_staged<K, RuntimeLayout><<<g, kHexThreads, smem, s>>>(words, out, n_elem, n_vars, ld, op, P, tab);
+        }
+    }
+    return launch_status();
+}
+
+int hex_launch(const unsigned long long* words, const float* raw, const float* m1d, int degree,
+               float* out, int64_t n_elem, int n_vars, int64_t ld, const vc3_layout* layout,
+               cudaStream_t s) {
+    if (degree < 1 || degree > 4 || n_elem < 0 || n_vars < 1 || n_vars > 65535 || ld < n_elem)
+        return VC3_ERR_ARG;
+    if (!m1d || !out || (!words && !raw)) return VC3_ERR_ARG;
+    if (!raw && !layout_ok(*layout)) return VC3_ERR_LAYOUT;
+    if (n_elem == 0) return VC3_OK;
+    HexOp op{};
+    for (int a = 0; a <= degree; ++a)
+        for (int b = 0; b <= degree; ++b) op.m[a][b] = m1d[a * (degree + 1) + b];
+    switch (degree) {
+        case 1: return hex_launch_k<1>(words, raw, out, n_elem, n_vars, ld, op, layout, s);
+        case 2: return hex_launch_k<2>(words, raw, out, n_elem, n_vars, ld, op, layout, s);
+        case 3: return hex_launch_k<3>(words, raw, out, n_elem, n_vars, ld, op, layout, s);
+        default: return hex_launch_k<4>(words, raw, out, n_elem, n_vars, ld, op, layout, s);
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -544,6 +784,20 @@ int vc3_fr_divergence_f32(const float* flux, const float* op, float* div, int64_
     if (!flux) return VC3_ERR_ARG;
     return fr_launch(nullptr, flux, op, div, n_elem, n_vars, ld, n_points, nullptr,
                      (cudaStream_t)stream);
+}
+
+int vc3_fr_divergence_hex(const uint64_t* words, const float* m1d, int degree, float* div,
+                          int64_t n_elem, int n_vars, int64_t ld, vc3_layout layout, void* stream) {
+    if (!words) return VC3_ERR_ARG;
+    return hex_launch((const unsigned long long*)words, nullptr, m1d, degree, div, n_elem, n_vars, ld,
+                      &layout, (cudaStream_t)stream);
+}
+
+int vc3_fr_divergence_hex_f32(const float* flux, const float* m1d, int degree, float* div,
+                              int64_t n_elem, int n_vars, int64_t ld, void* stream) {
+    if (!flux) return VC3_ERR_ARG;
+    return hex_launch(nullptr, flux, m1d, degree, div, n_elem, n_vars, ld, nullptr,
+                      (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -131,5 +131,53 @@ def flux_divergence_f32(flux, op: Operator, n_elem: int | None = None):
     return out
 
 
+def _hex_degree(ns: int) -> int:
+    k = round(ns ** (1.0 / 3.0)) - 1
+    if (k + 1) ** 3 != ns or not 1 <= k <= 4:
+        raise ValueError(f"{ns} points is not a hexahedron of degree 1..4")
+    return k
+
+
+def flux_divergence_hex(words, n_elem: int | None = None, layout=DEFAULT_LAYOUT, m1d=None):
+    """Sum-factorised divergence for tensor-product hexahedra (degree 1..4):
+    ``words`` CUDA uint64 ``[ns][n_vars][ld]`` with ns = (k+1)^3; the operator
+    is ``divergence_operator(k)`` unless ``m1d`` (the 1D derivative matrix)
+    is given.  Same result as ``flux_divergence`` to float32 rounding."""
+    layout = as_layout(layout)
+    lib = _native.load()
+    if not _dev.is_device(words) or words.dim() != 3:
+        raise ValueError("flux_divergence_hex takes a CUDA uint64 tensor [ns][n_vars][ld]")
+    w = words.contiguous()
+    ns, n_vars, ld = int(w.shape[0]), int(w.shape[1]), int(w.shape[2])
+    k = _hex_degree(ns)
+    m = np.ascontiguousarray(lagrange_derivative_matrix(gauss_legendre_nodes(k)) if m1d is None
+                             else m1d, dtype=np.float32)
+    n_elem = ld if n_elem is None else int(n_elem)
+    out = torch.empty((ns, n_vars, ld), dtype=torch.float32, device=w.device)
+    _native.check(lib.vc3_fr_divergence_hex(w.data_ptr(), m.ctypes.data, k, out.data_ptr(), n_elem,
+                                            n_vars, ld, _native.c_layout(layout), _dev.stream_of(w)),
+                  "fr_divergence_hex")
+    return out
+
+
+def flux_divergence_hex_f32(flux, n_elem: int | None = None, m1d=None):
+    """Float32 fluxes ``[ns][n_vars][ld][3]`` through the sum-factorised kernel."""
+    lib = _native.load()
+    if not _dev.is_device(flux) or flux.dim() != 4 or flux.shape[3] != 3:
+        raise ValueError("flux_divergence_hex_f32 takes a CUDA float32 tensor [ns][n_vars][ld][3]")
+    f = flux.to(torch.float32).contiguous()
+    ns, n_vars, ld = int(f.shape[0]), int(f.shape[1]), int(f.shape[2])
+    k = _hex_degree(ns)
+    m = np.ascontiguousarray(lagrange_derivative_matrix(gauss_legendre_nodes(k)) if m1d is None
+                             else m1d, dtype=np.float32)
+    n_elem = ld if n_elem is None else int(n_elem)
+    out = torch.empty((ns, n_vars, ld), dtype=torch.float32, device=f.device)
+    _native.check(lib.vc3_fr_divergence_hex_f32(f.data_ptr(), m.ctypes.data, k, out.data_ptr(), n_elem,
+                                                n_vars, ld, _dev.stream_of(f)),
+                  "fr_divergence_hex_f32")
+    return out
+
+
 __all__ = ["gauss_legendre_nodes", "lagrange_derivative_matrix", "divergence_operator",
-           "solution_points", "Operator", "flux_divergence", "flux_divergence_f32"]
+           "solution_points", "Operator", "flux_divergence", "flux_divergence_f32", "flux_divergence_hex",
+           "flux_divergence_hex_f32"]

@@ -93,3 +93,36 @@ def test_fr_divergence_physical_operator_and_layouts(oracle, vc3b, cuda):
                                  op, layout=lay).cpu().numpy()
         ref, scale = _reference(D, X)
         _check(got, ref, scale, lname)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k,n_elem,n_vars,pad", [(4, 1000, 5, 0), (1, 37, 2, 3), (2, 300, 3, 17),
+                                                  (3, 129, 1, 0)])
+def test_fr_divergence_hex_matches_dense(oracle, vc3b, cuda, k, n_elem, n_vars, pad):
+    """The sum-factorised hexahedron kernel == Alg. 1 with the dense operator."""
+    import torch
+
+    rng = np.random.default_rng(200 + k)
+    ns, ld = (k + 1) ** 3, n_elem + pad
+    F = rng.uniform(-2, 2, (ns, n_vars, ld, 3)).astype(np.float32)
+    F[:, :, 3::13] = 0.0
+    lay = vc3b.DEFAULT_LAYOUT
+    words = oracle.compress(F.reshape(-1, 3), lay, policy_by_code("SSS")).reshape(ns, n_vars, ld)
+    X = oracle.decompress(words.reshape(-1), lay).reshape(ns, n_vars, ld, 3)
+    D = fr.divergence_operator(k, dtype=np.float64)
+    # the kernel takes the float32 1D matrix: compare against the operator it implies
+    m32 = fr.lagrange_derivative_matrix(fr.gauss_legendre_nodes(k)).astype(np.float32)
+    D32 = fr.divergence_operator(k, dtype=np.float64)
+    n = k + 1
+    eye = np.eye(n)
+    M = m32.astype(np.float64)
+    D32 = np.concatenate([np.kron(eye, np.kron(eye, M)).T, np.kron(eye, np.kron(M, eye)).T,
+                          np.kron(M, np.kron(eye, eye)).T], axis=0)
+    assert np.abs(D32 - D).max() < 1e-5
+    got = fr.flux_divergence_hex(torch.from_numpy(words.view(np.int64)).cuda().view(torch.uint64),
+                                 n_elem).cpu().numpy()
+    ref, scale = _reference(D32, X[:, :, :n_elem])
+    _check(got[:, :, :n_elem], ref, scale, f"hex k={k}")
+    got32 = fr.flux_divergence_hex_f32(torch.from_numpy(F).cuda(), n_elem).cpu().numpy()
+    ref32, scale32 = _reference(D32, F[:, :, :n_elem])
+    _check(got32[:, :, :n_elem], ref32, scale32, f"hex f32 k={k}")

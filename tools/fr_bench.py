@@ -29,6 +29,12 @@ def main(k=4, n_elem=1 << 18, n_vars=5):
     rows = n_elem * n_vars
     t_c = timeit(lambda: fr.flux_divergence(words, op))
     t_f = timeit(lambda: fr.flux_divergence_f32(F, op))
+    if k <= 4:
+        t_hc = timeit(lambda: fr.flux_divergence_hex(words))
+        t_hf = timeit(lambda: fr.flux_divergence_hex_f32(F))
+        for name, t, b in (("hex-comp", t_hc, ns * 12), ("hex-f32", t_hf, ns * 16)):
+            print(f"{name:10s} k={k} n_elem={n_elem} {t*1e3:8.3f} ms  {rows/t/1e9:7.3f} G elem-eq/s  "
+                  f"{b*rows/t/1e9:7.1f} GB/s")
     flops = 2.0 * 3 * ns * ns * rows
     for name, t, b in (("compressed", t_c, 8 * 3 * 0 + ns * 8 + ns * 4), ("f32", t_f, ns * 12 + ns * 4)):
         print(f"{name:10s} k={k} n_elem={n_elem} {t*1e3:8.3f} ms  {rows/t/1e9:7.3f} G elem-eq/s  "
