@@ -519,34 +519,18 @@ int fr_launch(const unsigned long long* words, const float* raw, const float* bp
 // points per direction, point index p = px + n py + n^2 pz), Alg. 1 reduces to
 //   div[k] = sum_a M[kx][a] X_(a,ky,kz).x + M[ky][a] X_(kx,a,kz).y
 //                                        + M[kz][a] X_(kx,ky,a).z,
-// 3(k+1) multiply-adds per output instead of 3 ns.  One thread per
-// (element, equation) streams its ns words in point order, decodes each once
-// and scatters its three components into the ns accumulators held in
-// registers (indices are compile-time: the point loop is fully unrolled).
-// No shared-memory staging and no tensor cores: the kernel is bound by HBM
-// and the decode, which is where the paper's compression argument applies.
+// 3(k+1) multiply-adds per output instead of 3 ns.  fp32 fluxes: one thread
+// per (element, equation) streams its ns points in order and scatters the
+// three components into ns accumulators held in registers (indices are
+// compile-time: the point loop is fully unrolled); HBM-bound.
 struct HexOp {
     float m[6][6];
 };
 
-template <int K, bool RAW, class LAY>
-__global__ void __launch_bounds__(128) k_fr_hex(const unsigned long long* __restrict__ words,
-                                                const float* __restrict__ raw, float* __restrict__ out,
-                                                int64_t n_elem, int n_vars, int64_t ld, HexOp op,
-                                                Params Pin, const double2* __restrict__ gtab) {
+template <int K>
+__global__ void __launch_bounds__(128) k_fr_hex_f32(const float* __restrict__ raw, float* __restrict__ out,
+                                                    int64_t n_elem, int n_vars, int64_t ld, HexOp op) {
     constexpr int N1 = K + 1, NS = N1 * N1 * N1, PF = 8;
-    Params P = Pin;
-    LAY::apply(P);
-    extern __shared__ float2 s_tabf[];
-    if (!RAW) {
-        for (int t = threadIdx.x; t < P.tab_n; t += blockDim.x) {
-            const double2 e = gtab[t];
-            s_tabf[t] = make_float2((float)e.x, (float)e.y);
-        }
-        __syncthreads();
-    }
-    const float2* tt = s_tabf;
-    const float2* tp = s_tabf + P.p_base;
     const int c = blockIdx.y;
     const int64_t plane = (int64_t)n_vars * ld;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_elem;
@@ -555,32 +539,18 @@ __global__ void __launch_bounds__(128) k_fr_hex(const unsigned long long* __rest
         float acc[NS];
 #pragma unroll
         for (int k = 0; k < NS; ++k) acc[k] = 0.0f;
-        unsigned long long pw[PF];
-        float3 pf[PF];
+        float3 pf[PF];  // the next PF points' fluxes are in flight
 #pragma unroll
         for (int q = 0; q < PF; ++q) {
-            if (RAW) {
-                const float* p = raw + 3 * (base + q * plane);
-                pf[q] = make_float3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
-            } else {
-                pw[q] = __ldg(words + base + q * plane);
-            }
+            const float* p = raw + 3 * (base + q * plane);
+            pf[q] = make_float3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
         }
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
-            float x, y, z;
-            if (RAW) {
-                x = pf[j % PF].x; y = pf[j % PF].y; z = pf[j % PF].z;
-            } else {
-                decode_f32<LAY>(pw[j % PF], P, tt, tp, x, y, z);
-            }
+            const float x = pf[j % PF].x, y = pf[j % PF].y, z = pf[j % PF].z;
             if (j + PF < NS) {
-                if (RAW) {
-                    const float* p = raw + 3 * (base + (j + PF) * plane);
-                    pf[j % PF] = make_float3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
-                } else {
-                    pw[j % PF] = __ldg(words + base + (j + PF) * plane);
-                }
+                const float* p = raw + 3 * (base + (j + PF) * plane);
+                pf[j % PF] = make_float3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
             }
             const int jx = j % N1, jy = (j / N1) % N1, jz = j / (N1 * N1);
 #pragma unroll
@@ -596,8 +566,9 @@ __global__ void __launch_bounds__(128) k_fr_hex(const unsigned long long* __rest
     }
 }
 
-// Compressed fluxes: the per-thread decode above is latency-bound (all ns
-// accumulators live in registers, 2 warps per scheduler).  Here a CTA takes
+// Compressed fluxes: decoding inside that register-heavy loop is latency-bound
+// (measured 0.67 G elem-eq/s at k = 4: all ns accumulators live in registers,
+// 2 warps per scheduler).  Here a CTA takes
 // 32 elements of one equation: phase A decodes the tile's 32 x ns words with
 // all 8 warps (loads issued up front, lane = element) into shared memory as
 // [dimension][point][element] floats; phase B applies the sum-factorised
@@ -713,7 +684,7 @@ int hex_launch_k(const unsigned long long* words, const float* raw, float* out, 
     if (blocks > cap) blocks = cap;
     const dim3 grid((unsigned)blocks, (unsigned)n_vars);
     if (raw) {
-        k_fr_hex<K, true, RuntimeLayout><<<grid, 128, 0, s>>>(nullptr, raw, out, n_elem, n_vars, ld, op, P, tab);
+        k_fr_hex_f32<K><<<grid, 128, 0, s>>>(raw, out, n_elem, n_vars, ld, op);
     } else {
         constexpr int NS = (K + 1) * (K + 1) * (K + 1);
         smem += (size_t)3 * NS * kHexE * sizeof(float);
