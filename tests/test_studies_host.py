@@ -25,3 +25,14 @@ def test_report_envelope():
     doc = analysis.report(dom, DEFAULT_LAYOUT, DEFAULT_POLICY, extra=1)
     assert doc == {"layout": str(DEFAULT_LAYOUT), "policy": DEFAULT_POLICY.spec(),
                    "domain": "shell:0.5:2", "seed": 4, "count": 10, "extra": 1}
+
+
+def test_criterion_4b_joint_coding_exact():
+    """Acceptance 4b (pkg/tests/test_acceptance.py): exhaustive p = 8 joint round trip."""
+    import numpy as np
+
+    cfg = analysis.SplitConfig(8, 11)
+    nt, nph = np.meshgrid(np.arange(cfg.n_theta_max + 1), np.arange(cfg.n_phi_max + 1))
+    joint = analysis.joint_encode(nt.ravel(), nph.ravel(), cfg)
+    nt2, nph2 = analysis.joint_decode(joint, cfg)
+    assert joint.max() < 256 and np.array_equal(nt2, nt.ravel()) and np.array_equal(nph2, nph.ravel())
