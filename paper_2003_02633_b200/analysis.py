@@ -24,7 +24,7 @@ import numpy as np
 from . import _dev, _native
 from ._dev import torch
 from .codec import compress, decompress
-from .errors import EmptyDomain
+from .errors import DomainError, EmptyDomain, InvalidSplit  # noqa: F401
 from .layout import (  # noqa: F401  (the reference's analysis namespace)
     ALL_SINGLE_POLICY,
     DEFAULT_LAYOUT,

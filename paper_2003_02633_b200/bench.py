@@ -20,6 +20,7 @@ import numpy as np
 
 from . import _dev
 from ._dev import torch
+from .errors import LengthMismatch  # noqa: F401  (the reference's bench namespace)
 from .layout import ALL_SINGLE_POLICY, DEFAULT_LAYOUT, BitLayout, PrecisionPolicy, as_layout, as_policy
 from .ops import (  # noqa: F401
     COMPRESSED_BYTES_PER_ELEMENT,
@@ -68,6 +69,9 @@ class BenchResult:
         return self.__dict__.copy()
 
 
+from .analysis import SampleDomain  # noqa: E402,F401  (the reference's bench namespace)
+
+
 def llc_bytes() -> int | None:
     """L2 size of the current CUDA device, or None without one."""
     if torch is None or not torch.cuda.is_available():
@@ -94,8 +98,6 @@ def _median_time_ns(fn, repeats: int) -> float:
 def _vectors(n: int, seed: int, stream: int):
     """The reference's cube sample for operand ``stream`` (bench.py:149-155),
     drawn chunk by chunk and uploaded."""
-    from .analysis import SampleDomain
-
     dom = SampleDomain("cube", n, (seed << 1) | stream)
     out = torch.empty((n, 3), dtype=torch.float32, device=torch.device("cuda", torch.cuda.current_device()))
     pos = 0

@@ -19,7 +19,7 @@ import numpy as np
 from . import _dev, _native
 from ._dev import torch
 from .errors import NonFiniteInput
-from .layout import DEFAULT_LAYOUT, DEFAULT_POLICY, as_layout, as_policy
+from .layout import DEFAULT_LAYOUT, DEFAULT_POLICY, BitLayout, PrecisionPolicy, as_layout, as_policy  # noqa: F401
 
 __all__ = [
     "SphericalTriple",

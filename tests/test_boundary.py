@@ -78,3 +78,29 @@ def test_no_oracle_on_product_path():
     for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cuh")):
         text = f.read_text()
         assert "vc3_oracle" not in text and "oracle/" not in text, f
+
+
+def test_python_api_surface_matches_reference():
+    """Every public name of the reference package's modules exists here, and
+    every reference function's parameters are a prefix of ours (same names,
+    same order).  tests/golden/api_surface.json is recorded from the
+    reference by tests/golden/make_api_surface.py."""
+    import importlib
+    import inspect
+    import json
+    from pathlib import Path
+
+    surface = json.loads((Path(__file__).parent / "golden" / "api_surface.json").read_text())
+    problems = []
+    for mod_name, entries in surface.items():
+        ours = importlib.import_module(mod_name.replace("vc3", "paper_2003_02633_b200", 1))
+        for name, params in entries.items():
+            if not hasattr(ours, name):
+                problems.append(f"{mod_name}.{name} missing")
+                continue
+            obj = getattr(ours, name)
+            if params is not None and inspect.isfunction(obj):
+                mine = list(inspect.signature(obj).parameters)
+                if mine[: len(params)] != params:
+                    problems.append(f"{mod_name}.{name}{tuple(params)} vs ours {tuple(mine)}")
+    assert not problems, problems
