@@ -45,9 +45,10 @@ constexpr int kHalf = 128;
 constexpr int kPts = 8;                // solution points per K stage
 constexpr int kDecodeWarps = 16;       // 2 threads per element, 4 points each
 constexpr int kEpiWarps = 4;           // TMEM -> global, one per TMEM lane quarter
-constexpr int kThreadsFr = (kDecodeWarps + kEpiWarps + 2) * 32;
+constexpr int kThreadsFr = (kDecodeWarps + kEpiWarps + 3) * 32;
 constexpr int kLoadWarp = kDecodeWarps + kEpiWarps;
 constexpr int kMmaWarp = kDecodeWarps + kEpiWarps + 1;
+constexpr int kRawWarp = kDecodeWarps + kEpiWarps + 2;  // flux rows -> shared memory (BULK)
 constexpr int kASliceBytes = kHalf * kPts * 4;  // one half, one dimension, hi or lo: 4 KB
 
 __host__ __device__ constexpr int b_slice_bytes(int npad) { return npad * kPts * 4; }
@@ -214,23 +215,33 @@ struct FrArgs {
     const float* bprep;               // k_fr_prepare output
     float* out;                       // [ns][n_vars][ld]
     int64_t n_elem, ld;
-    int n_vars, ns, npad, nst, nbuf;
+    int n_vars, ns, npad, nst, nbuf, nraw;
 };
 
-template <bool RAW, bool TABLE, class LAY>
+// BULK: the flux rows of each stage (8 points x 256 elements, contiguous per
+// point) are brought into a shared-memory ring by cp.async.bulk from one
+// producer thread, so the decode warps never wait on HBM latency; otherwise
+// (strides not 16-byte aligned) the decode warps prefetch into registers.
+template <bool RAW, bool TABLE, bool BULK, class LAY>
 __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, const double2* __restrict__ gtab) {
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ __align__(1024) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int sbytes = stage_bytes(a.npad);
+    constexpr int esize = RAW ? 12 : 8;
+    constexpr int rbytes = kPts * kRows * esize;  // one raw-ring slot
     unsigned char* stages = smem;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)a.nbuf * sbytes);
+    unsigned char* rawbuf = smem + (size_t)a.nbuf * sbytes;
+    unsigned char* meta = rawbuf + (BULK ? (size_t)a.nraw * rbytes : 0);
+    uint64_t* full = reinterpret_cast<uint64_t*>(meta);
     uint64_t* empty = full + a.nbuf;
     uint64_t* acc_full = empty + a.nbuf;  // [2]
     uint64_t* acc_empty = acc_full + 2;   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
-    float2* s_tab = reinterpret_cast<float2*>(smem + (size_t)a.nbuf * sbytes + 1024);
+    uint64_t* raw_full = acc_empty + 2;   // [nraw]
+    uint64_t* raw_empty = raw_full + 8;   // [nraw]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 8);
+    float2* s_tab = reinterpret_cast<float2*>(meta + 1024);
     // accumulators: [buffer][half] x npad fp32 columns; two buffers when they fit
     const int nacc = 4 * a.npad <= 512 ? 2 : 1;
     const uint32_t tmem_cols = nacc * 2 * a.npad <= 256 ? 256 : 512;
@@ -246,6 +257,12 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], kEpiWarps);
+        }
+        if (BULK) {
+            for (int r = 0; r < a.nraw; ++r) {
+                mbar_init(&raw_full[r], 1);
+                mbar_init(&raw_empty[r], kDecodeWarps);
+            }
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -274,7 +291,8 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
         const float2* tp = s_tab + P.p_base;
         const int64_t plane = (int64_t)a.n_vars * a.ld;  // stride between solution points
         const int64_t plane2 = 2 * plane, plane3 = 3 * plane, step = (int64_t)kPts * plane;
-        // fetch cursor: runs two stages ahead of the decode, across tile boundaries
+        // register fetch cursor (!BULK): runs two stages ahead of the decode,
+        // across tile boundaries
         int64_t ftile = blockIdx.x;
         int fstage = 0;
         const unsigned long long* wp = nullptr;
@@ -288,7 +306,6 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
             wp = a.words + (RAW ? 0 : base);
             fp = a.raw + (RAW ? 3 * base : 0);
         };
-        begin_tile(ftile);
         unsigned long long w1[4], w2[4];
         float3 f1[4], f2[4];
         auto fetch = [&](unsigned long long* w, float3* f) {
@@ -313,20 +330,44 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
                 begin_tile(ftile);
             }
         };
-        fetch(w1, f1);
-        fetch(w2, f2);
+        if (!BULK) {
+            begin_tile(ftile);
+            fetch(w1, f1);
+            fetch(w2, f2);
+        }
         const int off = canon_off(row & (kHalf - 1), 4 * h);
-        int b = 0, use = 0;  // ring slot and how often it has been filled before
+        int b = 0, use = 0;  // A-ring slot and how often it has been filled before
+        int r = 0, ruse = 0; // raw-ring slot (BULK)
         for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             for (int s = 0; s < a.nst; ++s) {
                 unsigned long long w[4];
                 float3 f[4];
+                if (BULK) {
+                    // points 8s + 4h + q of this element from the raw ring
+                    const int nv = min(max(a.ns - (s * kPts + 4 * h), 0), 4);
+                    mbar_wait(&raw_full[r], ruse & 1);
+                    const unsigned char* rb = rawbuf + (size_t)r * rbytes;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    w[q] = w1[q]; f[q] = f1[q];
-                    w1[q] = w2[q]; f1[q] = f2[q];
+                    for (int q = 0; q < 4; ++q) {
+                        const unsigned char* e = rb + ((size_t)(4 * h + q) * kRows + row) * esize;
+                        if (RAW) {
+                            const float* ef = reinterpret_cast<const float*>(e);
+                            f[q] = q < nv ? make_float3(ef[0], ef[1], ef[2]) : make_float3(0.f, 0.f, 0.f);
+                        } else {
+                            w[q] = q < nv ? *reinterpret_cast<const unsigned long long*>(e) : 0ull;
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&raw_empty[r]);
+                    if (++r == a.nraw) { r = 0; ++ruse; }
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        w[q] = w1[q]; f[q] = f1[q];
+                        w1[q] = w2[q]; f1[q] = f2[q];
+                    }
+                    fetch(w2, f2);
                 }
-                fetch(w2, f2);
                 float x[4], y[4], z[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
@@ -411,6 +452,34 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
             }
         }
         __syncwarp();
+    } else if (BULK && warp == kRawWarp) {
+        // ---------------- flux rows (HBM -> smem ring, bulk async copy) ----------------
+        if (lane == 0) {
+            const int64_t plane = (int64_t)a.n_vars * a.ld;
+            const unsigned char* src0 = RAW ? reinterpret_cast<const unsigned char*>(a.raw)
+                                            : reinterpret_cast<const unsigned char*>(a.words);
+            int r = 0, ruse = 0;
+            for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int c = (int)(t / tiles_per_var);
+                const int64_t i0 = (t - (int64_t)c * tiles_per_var) * kRows;
+                const int64_t cnt = a.ld - i0 < kRows ? a.ld - i0 : kRows;  // rows are ld long
+                const uint32_t row_bytes = (uint32_t)(cnt * esize);
+                for (int s = 0; s < a.nst; ++s) {
+                    if (ruse > 0) mbar_wait(&raw_empty[r], (ruse - 1) & 1);
+                    const int nrows = min(kPts, a.ns - s * kPts);
+                    unsigned char* dst = rawbuf + (size_t)r * rbytes;
+                    mbar_arrive_tx(&raw_full[r], (uint32_t)nrows * row_bytes);
+                    for (int jj = 0; jj < nrows; ++jj) {
+                        const int64_t j = (int64_t)s * kPts + jj;
+                        bulk_g2s(dst + (size_t)jj * kRows * esize,
+                                 src0 + ((j * plane) + (int64_t)c * a.ld + i0) * esize, row_bytes,
+                                 &raw_full[r]);
+                    }
+                    if (++r == a.nraw) { r = 0; ++ruse; }
+                }
+            }
+        }
+        __syncwarp();
     } else if (warp == kMmaWarp) {
         // ---------------- MMA issue (one thread) ----------------
         if (lane == 0) {
@@ -489,28 +558,49 @@ int fr_launch(const unsigned long long* words, const float* raw, const float* bp
     }
     const size_t sb = (size_t)stage_bytes(a.npad);
     const size_t budget = 227 * 1024 - 1024 - tab_bytes;
+    // the raw ring needs 16-byte aligned rows: base pointer, ld multiple of 4
+    const int esize = raw ? 12 : 8;
+    const void* src = raw ? (const void*)raw : (const void*)words;
+    const size_t rbytes = (size_t)kPts * kRows * esize;
+    bool bulk = ((uintptr_t)src & 15u) == 0 && (ld % 4) == 0;
+    // two A/B stages (decode of s+1 overlaps the MMA of s) come first, more
+    // when they fit beside a raw ring of >= 2 slots; the ring takes the rest
     int nbuf = (int)(budget / sb);
-    if (nbuf > 4) nbuf = 4;
     if (nbuf > a.nst) nbuf = a.nst;
     if (nbuf < 1) return VC3_ERR_ARG;
+    const int nbuf2 = nbuf < 2 ? nbuf : 2;
+    int more = budget > 3 * rbytes ? (int)((budget - 3 * rbytes) / sb) : 0;
+    if (more > 4) more = 4;
+    if (more > a.nst) more = a.nst;
+    nbuf = more > nbuf2 ? more : nbuf2;
+    int nraw = (int)((budget - (size_t)nbuf * sb) / rbytes);
+    if (nraw > 8) nraw = 8;
+    if (nraw < 2) bulk = false;
     a.nbuf = nbuf;
-    const size_t smem = (size_t)nbuf * sb + 1024 + tab_bytes;
+    a.nraw = bulk ? nraw : 0;
+    const size_t smem = (size_t)nbuf * sb + (size_t)a.nraw * rbytes + 1024 + tab_bytes;
     const int64_t tiles = ((n_elem + kRows - 1) / kRows) * n_vars;
     const int64_t grid = tiles < sm_count() ? tiles : sm_count();  // persistent: one CTA per SM
-    const void* fn;
-    if (raw) fn = (const void*)k_fr_div<true, false, RuntimeLayout>;
-    else if (is_default_layout(*layout)) fn = (const void*)k_fr_div<false, true, DefaultLayout>;
-    else if (P.table_mode) fn = (const void*)k_fr_div<false, true, RuntimeLayout>;
-    else fn = (const void*)k_fr_div<false, false, RuntimeLayout>;
-    int st = ensure_smem(fn, smem);
-    if (st) return st;
-    if (raw) k_fr_div<true, false, RuntimeLayout><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P, tab);
-    else if (is_default_layout(*layout))
-        k_fr_div<false, true, DefaultLayout><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P, tab);
-    else if (P.table_mode)
-        k_fr_div<false, true, RuntimeLayout><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P, tab);
-    else
-        k_fr_div<false, false, RuntimeLayout><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P, tab);
+#define VC3_FR_GO(R, T, B, L)                                                            \
+    do {                                                                                 \
+        const int st_ = ensure_smem((const void*)k_fr_div<R, T, B, L>, smem);            \
+        if (st_) return st_;                                                             \
+        k_fr_div<R, T, B, L><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P, tab);        \
+    } while (0)
+    if (raw) {
+        if (bulk) VC3_FR_GO(true, false, true, RuntimeLayout);
+        else VC3_FR_GO(true, false, false, RuntimeLayout);
+    } else if (is_default_layout(*layout)) {
+        if (bulk) VC3_FR_GO(false, true, true, DefaultLayout);
+        else VC3_FR_GO(false, true, false, DefaultLayout);
+    } else if (P.table_mode) {
+        if (bulk) VC3_FR_GO(false, true, true, RuntimeLayout);
+        else VC3_FR_GO(false, true, false, RuntimeLayout);
+    } else {
+        if (bulk) VC3_FR_GO(false, false, true, RuntimeLayout);
+        else VC3_FR_GO(false, false, false, RuntimeLayout);
+    }
+#undef VC3_FR_GO
     return launch_status();
 }
 
