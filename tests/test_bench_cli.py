@@ -23,3 +23,22 @@ def test_reference_arm_prints_contract_line():
     assert d["e2e"] == {"value": d["value"], "unit": "Gvec/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
     assert d["metric"].startswith("compressed float3 vector-add")
+
+
+def test_reference_arm_under_torchrun_rank0_only():
+    """N > 1 (the driver's scaling launch): rank 0 alone runs and prints; the
+    other ranks exit 0 without output.  gloo on CPU, two ranks."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                          "--master-port", str(port), str(ROOT / "bench.py"), "--impl", "reference",
+                          "--gpus", "2", "--steps", "2", "--warmup", "1", "--cpu-sample", "65536"],
+                         capture_output=True, text=True, check=True, timeout=600)
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
