@@ -90,3 +90,23 @@ def test_gpu_codec_on_file_path(golden, vc3b, oracle, cuda, tmp_path):
     out, lay2 = decompress_stream(tmp_path / "m.vc3")
     assert lay2 == DEFAULT_LAYOUT
     assert np.array_equal(out, oracle.decompress(words, DEFAULT_LAYOUT))
+
+
+@pytest.mark.gpu
+def test_gpu_stream_device_tensors(golden, oracle, cuda, tmp_path):
+    """Device tensors on the file path: compress a CUDA tensor straight into a
+    stream, read it back onto the GPU."""
+    import torch
+
+    from paper_2003_02633_b200 import ALL_SINGLE_POLICY
+    from paper_2003_02633_b200.stream import compress_to_stream, decompress_stream
+
+    want = golden["cw_17_18_SSS_mixed"]
+    v = torch.from_numpy(golden["vec_mixed"][: want.size]).cuda()
+    n = compress_to_stream(tmp_path / "d.vc3", v, policy=ALL_SINGLE_POLICY)
+    words, _ = read_stream(tmp_path / "d.vc3")
+    assert n == want.size and np.array_equal(words, want)
+    out, lay = decompress_stream(tmp_path / "d.vc3", device="cuda")
+    assert out.is_cuda and lay == DEFAULT_LAYOUT
+    assert np.array_equal(out.cpu().numpy().view(np.uint32),
+                          oracle.decompress(words, DEFAULT_LAYOUT).view(np.uint32))
