@@ -319,6 +319,24 @@ def run_secondary(args, vc3b, lib, dev, stream, n):
     del q, dq, R, qf, dqf, Rf, vel
     torch.cuda.empty_cache()
 
+    # C4 at the paper's mesh size (800 elements x 125 points = 10^5 vectors):
+    # one full LSRK step, five eager launches vs one CUDA-graph replay
+    from paper_2003_02633_b200 import ops
+
+    ms_, vs_ = fields.icv_fields(800, 30.0, device=dev)
+    qs = vc3b.compress(ms_, lay, pol)
+    dqs = vc3b.compress(vs_ * 1e-3, lay, pol)
+    Rs = vc3b.compress(vs_, lay, pol)
+    stp = ops.LSRKStep(qs, dqs, Rs, 1e-3, lay, pol).capture()
+    reps = 200
+    stp.step(); stp.step_eager()
+    torch.cuda.synchronize()
+    te_ = time_region(stp.step_eager, reps, stream, torch)
+    tg_ = time_region(stp.step, reps, stream, torch)
+    out["C4_rk_stage_icv"]["paper_mesh_lsrk_step_us"] = {
+        "n_points": int(qs.numel()), "eager_5_launches": te_ * 1e3, "cuda_graph": tg_ * 1e3}
+    del ms_, vs_, qs, dqs, Rs, stp
+
     # C6: FR flux divergence (Alg. 1) on the tcgen05 kernel,
     # degree-4 hexahedra, 5 equation rows per point, compressed vs float32 fluxes
     from paper_2003_02633_b200 import fr

@@ -419,3 +419,27 @@ def test_fused_ops_other_layouts_vs_oracle(vc3b, oracle, cuda, lname, code):
                        oracle.axpy(al, a, b, lay, pol), lay, code, f"axpy {lname}")
     assert_vectors_match(vc3b.decompress(ta, lay).cpu().numpy(), oracle.decompress(a, lay),
                          f"decompress {lname}")
+
+
+@pytest.mark.gpu
+def test_lsrk_step_graph_matches_eager(vc3b, cuda):
+    """A CUDA-graph-captured LSRK step (5 rk_stage launches) is bit-identical
+    to the eager stages, over several steps."""
+    import torch
+
+    from paper_2003_02633_b200 import fields, ops
+
+    mom, vel = fields.icv_fields(800, 30.0, device="cuda")
+    pol = vc3b.ALL_SINGLE_POLICY
+    q0 = vc3b.compress(mom, vc3b.DEFAULT_LAYOUT, pol)
+    dq0 = vc3b.compress(vel * 1e-3, vc3b.DEFAULT_LAYOUT, pol)
+    R = vc3b.compress(vel, vc3b.DEFAULT_LAYOUT, pol)
+    qa, dqa, qb, dqb = q0.clone(), dq0.clone(), q0.clone(), dq0.clone()
+    ga = ops.LSRKStep(qa, dqa, R, 1e-3).capture()
+    eb = ops.LSRKStep(qb, dqb, R, 1e-3)
+    for _ in range(3):
+        ga.step()
+        eb.step_eager()
+    torch.cuda.synchronize()
+    assert torch.equal(qa, qb) and torch.equal(dqa, dqb)
+    assert not torch.equal(qa, q0)
