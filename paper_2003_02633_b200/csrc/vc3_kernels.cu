@@ -2,12 +2,14 @@
 // extern "C" boundary declared in include/vc3_b200.h.
 //
 // Memory layout in HBM: compressed words are contiguous uint64
-// arrays moved as 16-byte ulonglong2 pairs; vectors are the caller's
-// array-of-structs float32 [n][3] moved as three 16-byte float4 per group of
-// four vectors.  Every kernel is a grid-stride streaming loop over a grid
-// sized to a multiple of the SM count; nothing uncompressed touches HBM in
-// the fused operations.  Decoding kernels first copy the layout's sin/cos
-// table (<= 20.5 KB) from global memory into shared memory.
+// arrays moved as 32-byte groups of four (sm_100 256-bit LDG/STG; 16-byte
+// pairs in the axpy / RK kernels); vectors are the caller's array-of-structs
+// float32 [n][3] moved as three 16-byte float4 per group of four vectors.
+// Every kernel is a grid-stride streaming loop over a grid sized to a
+// multiple of the SM count; nothing uncompressed touches HBM in the fused
+// operations.  Decoding kernels first copy the layout's sin/cos table (49 KB
+// at the default layout, opt-in shared memory) from global memory into
+// shared memory.
 #include <cuda_runtime.h>
 
 #include <cmath>
