@@ -211,6 +211,13 @@ constexpr int kThreads = 256;
 #ifndef VC3_DECOMP_STAGE
 #define VC3_DECOMP_STAGE 1
 #endif
+// decompress CTAs: the 49 KB table is shared by more threads per CTA
+#ifndef VC3_DECOMP_THREADS
+#define VC3_DECOMP_THREADS 512
+#endif
+#ifndef VC3_DECOMP_MIN_BLOCKS
+#define VC3_DECOMP_MIN_BLOCKS 2
+#endif
 
 
 // grid for `items` work items of one thread each: at most `per_sm` CTAs per
@@ -337,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_compress(con
 
 // K2 decompress: 4 words (32 B in, 48 B out) per thread per step.
 template <bool TABLE, class LAY>
-__global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_decompress(const unsigned long long* __restrict__ w,
+__global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_decompress(const unsigned long long* __restrict__ w,
                                                          float* __restrict__ xyz, int64_t n,
                                                          Params Pin, bool vec,
                                                          const double2* __restrict__ gtab) {
@@ -876,15 +883,24 @@ int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layo
     if (st) return st;
     auto W = (const unsigned long long*)words;
     const bool vec = aligned32(words) && aligned16(xyz);
-    const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
+    const int64_t items = vec ? (n + 3) / 4 : n;
+    int64_t blocks = (items + VC3_DECOMP_THREADS - 1) / VC3_DECOMP_THREADS;
+    const int64_t cap = (int64_t)sm_count() * 4;
+    const unsigned grid = (unsigned)(blocks > cap ? cap : (blocks < 1 ? 1 : blocks));
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t stage = VC3_DECOMP_STAGE ? (size_t)kThreads * 48 : 0;  // 1.5 KB per warp
+    const size_t stage = VC3_DECOMP_STAGE ? (size_t)VC3_DECOMP_THREADS * 48 : 0;  // 1.5 KB per warp
+    const void* fn = is_default_layout(layout) ? (const void*)k_decompress<true, DefaultLayout>
+                     : P.table_mode           ? (const void*)k_decompress<true, RuntimeLayout>
+                                              : (const void*)k_decompress<false, RuntimeLayout>;
+    const size_t smem = (P.table_mode ? table_smem(P) : 0) + stage;
+    st = ensure_smem(fn, smem);
+    if (st) return st;
     if (is_default_layout(layout))
-        VC3_LAUNCH_TABLE((k_decompress<true, DefaultLayout>), grid, table_smem(P) + stage, s, W, xyz, n, P, vec, tab);
+        k_decompress<true, DefaultLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab);
     else if (P.table_mode)
-        VC3_LAUNCH_TABLE((k_decompress<true, RuntimeLayout>), grid, table_smem(P) + stage, s, W, xyz, n, P, vec, tab);
+        k_decompress<true, RuntimeLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab);
     else
-        VC3_LAUNCH_TABLE((k_decompress<false, RuntimeLayout>), grid, stage, s, W, xyz, n, P, vec, tab);
+        k_decompress<false, RuntimeLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab);
     return launch_status();
 }
 
