@@ -211,6 +211,17 @@ constexpr int kThreads = 256;
 #ifndef VC3_DECOMP_STAGE
 #define VC3_DECOMP_STAGE 1
 #endif
+// grid caps in CTAs per SM for the streaming kernels (grid-stride beyond);
+// more CTAs than resident slots balance the tail across SMs (measured)
+#ifndef VC3_ADD_CTAS_PER_SM
+#define VC3_ADD_CTAS_PER_SM 48
+#endif
+#ifndef VC3_COMPRESS_CTAS_PER_SM
+#define VC3_COMPRESS_CTAS_PER_SM 48
+#endif
+#ifndef VC3_DECOMP_CTAS_PER_SM
+#define VC3_DECOMP_CTAS_PER_SM 4
+#endif
 // decompress CTAs: the 49 KB table is shared by more threads per CTA
 #ifndef VC3_DECOMP_THREADS
 #define VC3_DECOMP_THREADS 512
@@ -762,7 +773,7 @@ struct RunCompress {
     static int run(const float* x, uint64_t* w, int64_t n, const Params& P, bool def, int32_t* nf,
                    cudaStream_t s) {
         const bool vec = aligned16(x) && aligned32(w);
-        const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
+        const unsigned grid = grid_for(vec ? (n + 3) / 4 : n, VC3_COMPRESS_CTAS_PER_SM);
         if (def)
             k_compress<POL, true, DefaultLayout><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
         else if (P.t <= 29 && P.p <= 29)
@@ -780,7 +791,7 @@ struct RunAdd {
         auto A = (const unsigned long long*)a, B = (const unsigned long long*)b;
         auto C = (unsigned long long*)c;
         const bool vec = aligned32(a) && aligned32(b) && aligned32(c);
-        const unsigned grid = grid_for(vec ? (n + 3) / 4 : n);
+        const unsigned grid = grid_for(vec ? (n + 3) / 4 : n, VC3_ADD_CTAS_PER_SM);
         if (def)
             VC3_LAUNCH_TABLE((k_add<POL, true, DefaultLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab);
         else if (P.table_mode)
@@ -798,7 +809,7 @@ struct RunAxpy {
         auto X = (const unsigned long long*)x, Y = (const unsigned long long*)y;
         auto O = (unsigned long long*)yo;
         const bool vec = aligned16(x) && aligned16(y) && aligned16(yo);
-        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
+        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n, VC3_ADD_CTAS_PER_SM);
         if (def)
             VC3_LAUNCH_TABLE((k_axpy<POL, true, DefaultLayout>), grid, table_smem(P), s, al, X, Y, O, n, P, vec, tab);
         else if (P.table_mode)
@@ -816,7 +827,7 @@ struct RunRk {
         auto Q = (unsigned long long*)q, D = (unsigned long long*)dq;
         auto RR = (const unsigned long long*)R;
         const bool vec = aligned16(q) && aligned16(dq) && aligned16(R);
-        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n);
+        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n, VC3_ADD_CTAS_PER_SM);
         if (def)
             VC3_LAUNCH_TABLE((k_rk<POL, true, DefaultLayout>), grid, table_smem(P), s, ca, cb, dt, Q, D, RR, n, P, vec, tab);
         else if (P.table_mode)
@@ -885,7 +896,7 @@ int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layo
     const bool vec = aligned32(words) && aligned16(xyz);
     const int64_t items = vec ? (n + 3) / 4 : n;
     int64_t blocks = (items + VC3_DECOMP_THREADS - 1) / VC3_DECOMP_THREADS;
-    const int64_t cap = (int64_t)sm_count() * 4;
+    const int64_t cap = (int64_t)sm_count() * VC3_DECOMP_CTAS_PER_SM;
     const unsigned grid = (unsigned)(blocks > cap ? cap : (blocks < 1 ? 1 : blocks));
     cudaStream_t s = (cudaStream_t)stream;
     const size_t stage = VC3_DECOMP_STAGE ? (size_t)VC3_DECOMP_THREADS * 48 : 0;  // 1.5 KB per warp
