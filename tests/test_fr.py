@@ -126,3 +126,35 @@ def test_fr_divergence_hex_matches_dense(oracle, vc3b, cuda, k, n_elem, n_vars, 
     got32 = fr.flux_divergence_hex_f32(torch.from_numpy(F).cuda(), n_elem).cpu().numpy()
     ref32, scale32 = _reference(D32, F[:, :, :n_elem])
     _check(got32[:, :, :n_elem], ref32, scale32, f"hex f32 k={k}")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ns,n_elem,n_vars", [(1, 300, 2), (37, 513, 3), (256, 260, 1), (125, 0, 5)])
+def test_fr_divergence_generic_operator_shapes(oracle, vc3b, cuda, ns, n_elem, n_vars):
+    """Alg. 1 with any dense operator: non-cube point counts, the 256-point
+    maximum, an empty element range."""
+    import torch
+
+    rng = np.random.default_rng(ns + n_elem)
+    D = rng.standard_normal((3 * ns, ns)).astype(np.float32)
+    ld = max(n_elem, 1)
+    F = rng.uniform(-1, 1, (ns, n_vars, ld, 3)).astype(np.float32)
+    lay = vc3b.DEFAULT_LAYOUT
+    words = oracle.compress(F.reshape(-1, 3), lay, policy_by_code("SSS")).reshape(ns, n_vars, ld)
+    X = oracle.decompress(words.reshape(-1), lay).reshape(ns, n_vars, ld, 3)
+    op = fr.Operator(D)
+    got = fr.flux_divergence(torch.from_numpy(words.view(np.int64)).cuda().view(torch.uint64), op,
+                             n_elem).cpu().numpy()
+    if n_elem:
+        ref, scale = _reference(D, X[:, :, :n_elem])
+        _check(got[:, :, :n_elem], ref, scale, f"ns={ns}")
+
+
+def test_fr_operator_limits():
+    """The C ABI rejects operators beyond 256 points (no GPU needed)."""
+    from paper_2003_02633_b200 import _native
+
+    lib = _native.load()
+    assert lib.vc3_fr_operator_floats(256) > 0
+    assert lib.vc3_fr_operator_floats(257) == -1 and lib.vc3_fr_operator_floats(0) == -1
+    assert lib.vc3_fr_divergence_f32(None, None, None, 1, 1, 1, 125, None) == -2
