@@ -166,16 +166,19 @@ __device__ __forceinline__ void decode_f32(unsigned long long w, const Params& P
     const unsigned long long field = w >> (P.p + P.t);
     const int nt = (int)((unsigned)w & (unsigned)P.tmask);
     const int nph = (int)((unsigned)(w >> P.t) & (unsigned)P.pmask);
-    const bool endp = nt == (int)P.ntmax;
-    const int it = endp ? P.t_n - 1 : (nt >> P.t_shift);
-    const int lt = endp ? 0 : (nt & ((1 << P.t_shift) - 1));
-    const bool pole = nph == (int)P.npmax;
-    const int ip = pole ? P.p_n - 1 : (nph >> P.p_shift);
-    const int lp = pole ? 0 : (nph & ((1 << P.p_shift) - 1));
+    // no endpoint / pole entries needed at float32 accuracy: nt = ntmax and
+    // nph = npmax reach pi through the last grid entry plus the residual
     float st, ct, sp, cp;
-    sincos_tab_f(tab_t, it, lt, (float)P.t_delta, st, ct);
-    sincos_tab_f(tab_p, ip, lp, (float)P.p_delta, sp, cp);
-    const float r = decode_mag(field, P);  // exact float32 magnitude, 0 for a zero field
+    sincos_tab_f(tab_t, nt >> P.t_shift, nt & ((1 << P.t_shift) - 1), (float)P.t_delta, st, ct);
+    sincos_tab_f(tab_p, nph >> P.p_shift, nph & ((1 << P.p_shift) - 1), (float)P.p_delta, sp, cp);
+    float r;
+    if (P.dec_normal) {
+        // every exponent maps to a normal float32: re-bias the field's bits
+        const unsigned f = (unsigned)field & ((1u << (P.e + P.m)) - 1u);
+        r = field ? __uint_as_float((f << (23 - P.m)) + ((unsigned)(127 - P.bias) << 23)) : 0.0f;
+    } else {
+        r = decode_mag(field, P);  // exact float32 magnitude, 0 for a zero field
+    }
     ox = __fmul_rn(__fmul_rn(r, ct), sp);
     oy = __fmul_rn(__fmul_rn(r, st), sp);
     oz = __fmul_rn(r, cp);
