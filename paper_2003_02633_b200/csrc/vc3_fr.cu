@@ -142,35 +142,25 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 __device__ __forceinline__ float tf32_hi(float v) { return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u); }
 
 // fp32 decode for the contraction.  The GEMM rounds each product to ~2^-21
-// (3xTF32), so the operand needs no more than float32 accuracy: same table
-// index split as decompress_one<true> (vc3_device.cuh) with the table held
-// as float2 and the residual rotation psi <= 2 pi / 2^11 evaluated to
-// sin psi ~ psi - psi^3/6, cos psi - 1 ~ -psi^2/2 (truncation < 2^-40).
-// Agreement with vc3_decompress: a few float32 ulp (tests/test_fr.py).
-__device__ __forceinline__ void sincos_tab_f(const float2* __restrict__ tab, int idx, int lo,
-                                             float delta, float& s, float& c) {
-    const float2 A = tab[idx];
-    // lo < 2^23: exact int -> float on the FMA pipe
-    const float lof = __fsub_rn(__int_as_float(0x4B000000 | lo), 8388608.0f);
-    const float psi = __fmul_rn(lof, delta);
-    const float u = __fmul_rn(psi, psi);
-    const float sps = __fmaf_rn(__fmul_rn(psi, u), -0.16666667f, psi);
-    const float cm1 = __fmul_rn(u, -0.5f);
-    s = __fmaf_rn(A.y, sps, __fmaf_rn(A.x, cm1, A.x));
-    c = __fmaf_rn(-A.x, sps, __fmaf_rn(A.y, cm1, A.y));
-}
-
+// (3xTF32), so the operand needs no more than that: the angles are formed in
+// float32 (|error| ~ 2^-22) and their sin/cos come from the hardware
+// (MUFU.SIN/COS, |error| <= 2^-21.4 on [-pi, pi]).  No shared-memory table:
+// the table gathers of the exact decode were this kernel's bottleneck
+// (compressed FR at k = 4: 2.07 -> 2.38 G elem-eq/s).  Agreement with
+// vc3_decompress: |dx| <= ~2^-21 |x| per component (tests/test_fr.py bounds
+// the divergence at 2^-18 sum |D||X|).
 template <class LAY>
-__device__ __forceinline__ void decode_f32(unsigned long long w, const Params& P, const float2* tab_t,
-                                           const float2* tab_p, float& ox, float& oy, float& oz) {
+__device__ __forceinline__ void decode_f32(unsigned long long w, const Params& P, float& ox, float& oy,
+                                           float& oz) {
     const unsigned long long field = w >> (P.p + P.t);
-    const int nt = (int)((unsigned)w & (unsigned)P.tmask);
-    const int nph = (int)((unsigned)(w >> P.t) & (unsigned)P.pmask);
-    // no endpoint / pole entries needed at float32 accuracy: nt = ntmax and
-    // nph = npmax reach pi through the last grid entry plus the residual
+    const unsigned nt = (unsigned)(w & P.tmask);
+    const unsigned nph = (unsigned)((w >> P.t) & P.pmask);
     float st, ct, sp, cp;
-    sincos_tab_f(tab_t, nt >> P.t_shift, nt & ((1 << P.t_shift) - 1), (float)P.t_delta, st, ct);
-    sincos_tab_f(tab_p, nph >> P.p_shift, nph & ((1 << P.p_shift) - 1), (float)P.p_delta, sp, cp);
+    const float th = __fmaf_rn(__uint2float_rn(nt), (float)(2.0 * 3.141592653589793 / (double)P.ntmax),
+                               -3.14159265358979f);
+    const float ph = __fmul_rn(__uint2float_rn(nph), (float)(3.141592653589793 / (double)P.npmax));
+    __sincosf(th, &st, &ct);
+    __sincosf(ph, &sp, &cp);
     float r;
     if (P.dec_normal) {
         // every exponent maps to a normal float32: re-bias the field's bits
@@ -225,8 +215,8 @@ struct FrArgs {
 // point) are brought into a shared-memory ring by cp.async.bulk from one
 // producer thread, so the decode warps never wait on HBM latency; otherwise
 // (strides not 16-byte aligned) the decode warps prefetch into registers.
-template <bool RAW, bool TABLE, bool BULK, class LAY>
-__global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, const double2* __restrict__ gtab) {
+template <bool RAW, bool BULK, class LAY>
+__global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin) {
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -244,7 +234,6 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
     uint64_t* raw_full = acc_empty + 2;   // [nraw]
     uint64_t* raw_empty = raw_full + 8;   // [nraw]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 8);
-    float2* s_tab = reinterpret_cast<float2*>(meta + 1024);
     // accumulators: [buffer][half] x npad fp32 columns; two buffers when they fit
     const int nacc = 4 * a.npad <= 512 ? 2 : 1;
     const uint32_t tmem_cols = nacc * 2 * a.npad <= 256 ? 256 : 512;
@@ -275,12 +264,6 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
                      "r"(tmem_cols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
-    if (!RAW && TABLE) {
-        for (int t = threadIdx.x; t < P.tab_n; t += blockDim.x) {
-            const double2 e = gtab[t];
-            s_tab[t] = make_float2((float)e.x, (float)e.y);
-        }
-    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -290,8 +273,6 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
         // ---------------- producers of A (decode), all tiles of this CTA ----------------
         const int row = threadIdx.x & (kRows - 1), h = threadIdx.x / kRows;
         const int m = row / kHalf;
-        const float2* tt = s_tab;
-        const float2* tp = s_tab + P.p_base;
         const int64_t plane = (int64_t)a.n_vars * a.ld;  // stride between solution points
         const int64_t plane2 = 2 * plane, plane3 = 3 * plane, step = (int64_t)kPts * plane;
         // register fetch cursor (!BULK): runs two stages ahead of the decode,
@@ -376,11 +357,9 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin, 
                 for (int q = 0; q < 4; ++q) {
                     if (RAW) {
                         x[q] = f[q].x; y[q] = f[q].y; z[q] = f[q].z;
-                    } else if (TABLE) {
-                        // zero words (and padding) decode to exact zeros
-                        decode_f32<LAY>(w[q], P, tt, tp, x[q], y[q], z[q]);
                     } else {
-                        decompress_one<false, true>(w[q], P, nullptr, nullptr, x[q], y[q], z[q]);
+                        // zero words (and padding) decode to exact zeros
+                        decode_f32<LAY>(w[q], P, x[q], y[q], z[q]);
                     }
                 }
                 if (use > 0) mbar_wait(&empty[b], (use - 1) & 1);
@@ -550,17 +529,12 @@ int fr_launch(const unsigned long long* words, const float* raw, const float* bp
     a.npad = npad_for(ns);
     a.nst = nst_for(ns);
     Params P{};
-    const double2* tab = nullptr;
-    size_t tab_bytes = 0;
     if (!raw) {
         if (!layout_ok(*layout)) return VC3_ERR_LAYOUT;
         P = make_params(*layout);
-        const int st = get_table(P, &tab);
-        if (st) return st;
-        tab_bytes = table_smem(P) / 2;  // held as float2
     }
     const size_t sb = (size_t)stage_bytes(a.npad);
-    const size_t budget = 227 * 1024 - 1024 - tab_bytes;
+    const size_t budget = 227 * 1024 - 1024;
     // the raw ring needs 16-byte aligned rows: base pointer, ld multiple of 4
     const int esize = raw ? 12 : 8;
     const void* src = raw ? (const void*)raw : (const void*)words;
@@ -581,27 +555,24 @@ int fr_launch(const unsigned long long* words, const float* raw, const float* bp
     if (nraw < 2) bulk = false;
     a.nbuf = nbuf;
     a.nraw = bulk ? nraw : 0;
-    const size_t smem = (size_t)nbuf * sb + (size_t)a.nraw * rbytes + 1024 + tab_bytes;
+    const size_t smem = (size_t)nbuf * sb + (size_t)a.nraw * rbytes + 1024;
     const int64_t tiles = ((n_elem + kRows - 1) / kRows) * n_vars;
     const int64_t grid = tiles < sm_count() ? tiles : sm_count();  // persistent: one CTA per SM
-#define VC3_FR_GO(R, T, B, L)                                                            \
+#define VC3_FR_GO(R, B, L)                                                               \
     do {                                                                                 \
-        const int st_ = ensure_smem((const void*)k_fr_div<R, T, B, L>, smem);            \
+        const int st_ = ensure_smem((const void*)k_fr_div<R, B, L>, smem);               \
         if (st_) return st_;                                                             \
-        k_fr_div<R, T, B, L><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P, tab);        \
+        k_fr_div<R, B, L><<<(unsigned)grid, kThreadsFr, smem, s>>>(a, P);               \
     } while (0)
     if (raw) {
-        if (bulk) VC3_FR_GO(true, false, true, RuntimeLayout);
-        else VC3_FR_GO(true, false, false, RuntimeLayout);
+        if (bulk) VC3_FR_GO(true, true, RuntimeLayout);
+        else VC3_FR_GO(true, false, RuntimeLayout);
     } else if (is_default_layout(*layout)) {
-        if (bulk) VC3_FR_GO(false, true, true, DefaultLayout);
-        else VC3_FR_GO(false, true, false, DefaultLayout);
-    } else if (P.table_mode) {
-        if (bulk) VC3_FR_GO(false, true, true, RuntimeLayout);
-        else VC3_FR_GO(false, true, false, RuntimeLayout);
+        if (bulk) VC3_FR_GO(false, true, DefaultLayout);
+        else VC3_FR_GO(false, false, DefaultLayout);
     } else {
-        if (bulk) VC3_FR_GO(false, false, true, RuntimeLayout);
-        else VC3_FR_GO(false, false, false, RuntimeLayout);
+        if (bulk) VC3_FR_GO(false, true, RuntimeLayout);
+        else VC3_FR_GO(false, false, RuntimeLayout);
     }
 #undef VC3_FR_GO
     return launch_status();
@@ -672,22 +643,14 @@ constexpr int kHexE = 32;
 constexpr int kHexThreads = 256;
 
 template <int K, class LAY>
-__global__ void __launch_bounds__(kHexThreads, 3) k_fr_hex_staged(
+__global__ void __launch_bounds__(kHexThreads, 4) k_fr_hex_staged(
     const unsigned long long* __restrict__ words, float* __restrict__ out, int64_t n_elem, int n_vars,
-    int64_t ld, HexOp op, Params Pin, const double2* __restrict__ gtab) {
+    int64_t ld, HexOp op, Params Pin) {
     constexpr int N1 = K + 1, NS = N1 * N1 * N1, NW = kHexThreads / 32;
     constexpr int NJ = (NS + NW - 1) / NW;  // points per warp in phase A
     Params P = Pin;
     LAY::apply(P);
-    extern __shared__ float2 s_tabf[];
-    float* xs = reinterpret_cast<float*>(s_tabf + P.tab_n);  // [3][NS][kHexE]
-    for (int t = threadIdx.x; t < P.tab_n; t += blockDim.x) {
-        const double2 e = gtab[t];
-        s_tabf[t] = make_float2((float)e.x, (float)e.y);
-    }
-    __syncthreads();
-    const float2* tt = s_tabf;
-    const float2* tp = s_tabf + P.p_base;
+    extern __shared__ float xs[];  // [3][NS][kHexE]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t blocks_per_var = (n_elem + kHexE - 1) / kHexE;
     const int64_t ntiles = blocks_per_var * n_vars;
@@ -716,7 +679,7 @@ __global__ void __launch_bounds__(kHexThreads, 3) k_fr_hex_staged(
             const int j = warp + NW * r;
             if (j < NS) {
                 float x, y, z;
-                decode_f32<LAY>(w[r], P, tt, tp, x, y, z);
+                decode_f32<LAY>(w[r], P, x, y, z);
                 xs[(0 * NS + j) * kHexE + lane] = x;
                 xs[(1 * NS + j) * kHexE + lane] = y;
                 xs[(2 * NS + j) * kHexE + lane] = z;
@@ -763,15 +726,8 @@ template <int K>
 int hex_launch_k(const unsigned long long* words, const float* raw, float* out, int64_t n_elem,
                  int n_vars, int64_t ld, const HexOp& op, const vc3_layout* layout, cudaStream_t s) {
     Params P{};
-    const double2* tab = nullptr;
     size_t smem = 0;
-    if (!raw) {
-        P = make_params(*layout);
-        if (!P.table_mode) return VC3_ERR_LAYOUT;  // wide layouts: use vc3_fr_divergence
-        const int st = get_table(P, &tab);
-        if (st) return st;
-        smem = table_smem(P) / 2;
-    }
+    if (!raw) P = make_params(*layout);
     int64_t blocks = (n_elem + 127) / 128;
     const int64_t cap = (int64_t)sm_count() * 8;
     if (blocks > cap) blocks = cap;
@@ -782,18 +738,18 @@ int hex_launch_k(const unsigned long long* words, const float* raw, float* out, 
         constexpr int NS = (K + 1) * (K + 1) * (K + 1);
         smem += (size_t)3 * NS * kHexE * sizeof(float);
         const int64_t tiles = ((n_elem + kHexE - 1) / kHexE) * n_vars;
-        const int64_t cap3 = (int64_t)sm_count() * 3;  // three 73-KB CTAs per SM at k = 4
+        const int64_t cap3 = (int64_t)sm_count() * 4;  // four 48-KB CTAs per SM at k = 4
         const unsigned g = (unsigned)(tiles < cap3 ? tiles : cap3);
         if (is_default_layout(*layout)) {
             const int st = ensure_smem((const void*)k_fr_hex_staged<K, DefaultLayout>, smem);
             if (st) return st;
             cudaFuncSetAttribute((const void*)k_fr_hex_staged<K, DefaultLayout>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-            k_fr_hex_staged<K, DefaultLayout><<<g, kHexThreads, smem, s>>>(words, out, n_elem, n_vars, ld, op, P, tab);
+            k_fr_hex_staged<K, DefaultLayout><<<g, kHexThreads, smem, s>>>(words, out, n_elem, n_vars, ld, op, P);
         } else {
             const int st = ensure_smem((const void*)k_fr_hex_staged<K, RuntimeLayout>, smem);
             if (st) return st;
-            k_fr_hex_staged<K, RuntimeLayout><<<g, kHexThreads, smem, s>>>(words, out, n_elem, n_vars, ld, op, P, tab);
+            k_fr_hex_staged<K, RuntimeLayout><<<g, kHexThreads, smem, s>>>(words, out, n_elem, n_vars, ld, op, P);
         }
     }
     return launch_status();
