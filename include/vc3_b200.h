@@ -161,11 +161,22 @@ int vc3_variant_maxima(vc3_layout layout, vc3_variant variant, int64_t* n_theta_
 
 /* ---- statistics (analysis.py:118-167) ------------------------------------ */
 
-/* Per-chunk error moments of e_i = ||v_i - vh_i||_2 (optionally / ||v_i||), in
- * double: for chunk k (chunk vectors each, last one ragged) writes
- * d_chunk_stats[4k..4k+3] = (count, mean, M2, max).  Chunks merge on the host
- * (or across ranks) in chunk order exactly like analysis._Welford. */
-int vc3_error_stats(const float* v, const float* vh, int64_t n, int32_t normalised,
+/* Per-chunk error moments, in double: for chunk k (chunk vectors each, last
+ * one ragged) writes d_chunk_stats[4k..4k+3] = (count, mean, M2, max).
+ * Chunks merge on the host (or across ranks) in chunk order exactly like
+ * analysis._Welford.  kind selects the per-vector error e_i:
+ *   VC3_ERR_L2             ||v - vh||_2                 (analysis.py:148-154)
+ *   VC3_ERR_L2_NORMALISED  ||v - vh||_2 / ||v||_2        (normalised=True)
+ *   VC3_ERR_ANGULAR        atan2(||v x vh||, v . vh), radians
+ *   VC3_ERR_REL_MAGNITUDE  | ||vh|| - ||v|| | / ||v||
+ * The last two are not in the reference; their op order
+ * is fixed and restated on the CPU by the test suite.  0/1 keep the meaning of
+ * the reference's `normalised` flag. */
+#define VC3_ERR_L2 0
+#define VC3_ERR_L2_NORMALISED 1
+#define VC3_ERR_ANGULAR 2
+#define VC3_ERR_REL_MAGNITUDE 3
+int vc3_error_stats(const float* v, const float* vh, int64_t n, int32_t kind,
                     int64_t chunk, double* d_chunk_stats, void* stream);
 
 /* ---- flux-reconstruction flux divergence (Alg. 1) ------

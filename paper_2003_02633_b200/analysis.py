@@ -140,33 +140,51 @@ class ChunkMerger:
         return ErrorStats(self.mean, self.max, sd, self.n, normalised)
 
 
-def chunk_moments(v, vh, normalised: bool, chunk: int = CHUNK):
-    """Device K6 kernel: (k, 4) float64 tensor of per-chunk moments of
-    e = ||v - vh||_2 (optionally / ||v||) for CUDA tensors v, vh of shape (n, 3)."""
+# error metrics of the K6 kernel (include/vc3_b200.h VC3_ERR_*): "l2" is the
+# reference's (analysis.py:148-154); "angular" (radians) and
+# "relative_magnitude" are the harness metrics of SURVEY §8a R19
+METRICS = {"l2": 0, "angular": 2, "relative_magnitude": 3}
+
+
+def _kind(normalised: bool, metric: str) -> int:
+    if metric not in METRICS:
+        raise ValueError(f"unknown error metric {metric!r}; expected one of {sorted(METRICS)}")
+    return 1 if (metric == "l2" and normalised) else METRICS[metric]
+
+
+def chunk_moments(v, vh, normalised: bool, chunk: int = CHUNK, metric: str = "l2"):
+    """Device K6 kernel: (k, 4) float64 tensor of per-chunk (count, mean, M2,
+    max) of the per-vector error for CUDA tensors v, vh of shape (n, 3):
+    ||v - vh||_2 (optionally / ||v||), or the angle between v and vh, or the
+    relative magnitude error (``metric``)."""
     lib = _native.load()
     n = v.shape[0]
     k = max(1, (n + chunk - 1) // chunk)
     out = torch.zeros((k, 4), dtype=torch.float64, device=v.device)
-    _native.check(lib.vc3_error_stats(v.data_ptr(), vh.data_ptr(), n, int(bool(normalised)),
+    _native.check(lib.vc3_error_stats(v.data_ptr(), vh.data_ptr(), n, _kind(normalised, metric),
                                       chunk, out.data_ptr(), _dev.stream_of(v)), "error_stats")
     return out
 
 
-def _chunk_tuple(domain: SampleDomain, index: int, layout, policy, normalised: bool) -> np.ndarray:
+def _chunk_tuple(domain: SampleDomain, index: int, layout, policy, normalised: bool,
+                 metric: str = "l2") -> np.ndarray:
     v = _dev.upload(domain.chunk(index, domain.chunk_size(index)))
     vh = decompress(compress(v, layout, policy), layout)
-    return chunk_moments(v, vh, normalised, CHUNK)[0].cpu().numpy()
+    return chunk_moments(v, vh, normalised, CHUNK, metric)[0].cpu().numpy()
 
 
 def error_study(domain: SampleDomain, layout=DEFAULT_LAYOUT, policy=DEFAULT_POLICY,
-                normalised: bool = False) -> ErrorStats:
-    """Round-trip L2 error statistics over a sample domain (analysis.py:157-167)."""
+                normalised: bool = False, metric: str = "l2") -> ErrorStats:
+    """Round-trip error statistics over a sample domain (analysis.py:157-167).
+    ``metric`` "l2" (the reference's) or the harness metrics "angular" /
+    "relative_magnitude"."""
     if domain.count == 0:
         raise EmptyDomain("error_study needs at least one sample")
     layout, policy = as_layout(layout), as_policy(policy)
+    _kind(normalised, metric)
     acc = ChunkMerger()
     for i in range(domain.n_chunks()):
-        c = _chunk_tuple(domain, i, layout, policy, normalised)
+        c = _chunk_tuple(domain, i, layout, policy, normalised, metric)
         acc.add(int(c[0]), float(c[1]), float(c[2]), float(c[3]))
     return acc.stats(normalised)
 
@@ -180,7 +198,7 @@ def shard_range(n_items: int, rank: int, world: int) -> tuple[int, int]:
 
 def error_study_sharded(domain: SampleDomain, layout=DEFAULT_LAYOUT, policy=DEFAULT_POLICY,
                         normalised: bool = False, group=None,
-                        tuple_fn=None) -> ErrorStats:
+                        tuple_fn=None, metric: str = "l2") -> ErrorStats:
     """``error_study`` with chunks split over a torch.distributed group.
 
     The only exchange is an all-gather of the (count, mean, M2, max) tuples
@@ -196,7 +214,7 @@ def error_study_sharded(domain: SampleDomain, layout=DEFAULT_LAYOUT, policy=DEFA
     nch = domain.n_chunks()
     per = (nch + world - 1) // world
     lo, hi = shard_range(nch, rank, world)
-    fn = tuple_fn or (lambda d, i: _chunk_tuple(d, i, layout, policy, normalised))
+    fn = tuple_fn or (lambda d, i: _chunk_tuple(d, i, layout, policy, normalised, metric))
     mine = np.zeros((per, 4), dtype=np.float64)
     for j, i in enumerate(range(lo, hi)):
         mine[j] = fn(domain, i)

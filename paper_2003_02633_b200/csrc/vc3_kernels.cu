@@ -698,16 +698,33 @@ __device__ __forceinline__ Moments chan(Moments a, Moments b) {
     return r;
 }
 
-__device__ __forceinline__ double err_one(const float* v, const float* vh, int64_t i, int normalised) {
-    const double dx = (double)v[3 * i] - (double)vh[3 * i];
-    const double dy = (double)v[3 * i + 1] - (double)vh[3 * i + 1];
-    const double dz = (double)v[3 * i + 2] - (double)vh[3 * i + 2];
-    double e = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz)));
-    if (normalised) {
-        const double x = v[3 * i], y = v[3 * i + 1], z = v[3 * i + 2];
-        const double nv = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
-        e = __ddiv_rn(e, nv > 0.0 ? nv : 1.0);
+// Error metrics (include/vc3_b200.h VC3_ERR_*), double precision, every
+// operation rounded in the order written (the tests' numpy restatement
+// follows the same order):
+//   0 L2:        e = ||v - vh||
+//   1 L2/|v|:    e = ||v - vh|| / ||v||            (||v|| = 0 -> / 1)
+//   2 angular:   e = atan2(||v x vh||, v . vh)     (radians; 0 for zero vectors)
+//   3 rel. mag.: e = | ||vh|| - ||v|| | / ||v||    (||v|| = 0 -> 0)
+__device__ __forceinline__ double norm3(double x, double y, double z) {
+    return __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)), __dmul_rn(z, z)));
+}
+
+__device__ __forceinline__ double err_one(const float* v, const float* vh, int64_t i, int kind) {
+    const double x = v[3 * i], y = v[3 * i + 1], z = v[3 * i + 2];
+    const double a = vh[3 * i], b = vh[3 * i + 1], c = vh[3 * i + 2];
+    if (kind == VC3_ERR_ANGULAR) {
+        const double cx = __dsub_rn(__dmul_rn(y, c), __dmul_rn(z, b));
+        const double cy = __dsub_rn(__dmul_rn(z, a), __dmul_rn(x, c));
+        const double cz = __dsub_rn(__dmul_rn(x, b), __dmul_rn(y, a));
+        const double dot = __dadd_rn(__dadd_rn(__dmul_rn(x, a), __dmul_rn(y, b)), __dmul_rn(z, c));
+        return atan2(norm3(cx, cy, cz), dot);
     }
+    const double nv = norm3(x, y, z);
+    if (kind == VC3_ERR_REL_MAGNITUDE) {
+        return nv > 0.0 ? __ddiv_rn(fabs(__dsub_rn(norm3(a, b, c), nv)), nv) : 0.0;
+    }
+    double e = norm3(__dsub_rn(x, a), __dsub_rn(y, b), __dsub_rn(z, c));
+    if (kind == VC3_ERR_L2_NORMALISED) e = __ddiv_rn(e, nv > 0.0 ? nv : 1.0);
     return e;
 }
 
@@ -716,7 +733,7 @@ constexpr int kStatSlice = 8192;  // vectors per block slice
 
 __global__ void __launch_bounds__(kStatThreads) k_err_partial(const float* __restrict__ v,
                                                               const float* __restrict__ vh,
-                                                              int64_t n, int normalised,
+                                                              int64_t n, int kind,
                                                               int64_t chunk, int slices_per_chunk,
                                                               Moments* __restrict__ part) {
     const int64_t c = blockIdx.y, s = blockIdx.x;
@@ -724,7 +741,7 @@ __global__ void __launch_bounds__(kStatThreads) k_err_partial(const float* __res
     const int64_t lo = c0 + s * (int64_t)kStatSlice, hi = min(c1, lo + kStatSlice);
     Moments m = {0, 0, 0, 0};
     for (int64_t i = lo + threadIdx.x; i < hi; i += kStatThreads) {
-        const double e = err_one(v, vh, i, normalised);
+        const double e = err_one(v, vh, i, kind);
         m.n += 1;
         const double d = e - m.mean;
         m.mean += d / m.n;
@@ -1037,8 +1054,9 @@ int vc3_magnitude_events(const float* xyz, int64_t n, vc3_layout layout,
     return launch_status();
 }
 
-int vc3_error_stats(const float* v, const float* vh, int64_t n, int32_t normalised, int64_t chunk,
+int vc3_error_stats(const float* v, const float* vh, int64_t n, int32_t kind, int64_t chunk,
                     double* d_chunk_stats, void* stream) {
+    if (kind < VC3_ERR_L2 || kind > VC3_ERR_REL_MAGNITUDE) return VC3_ERR_ARG;
     VC3_CHECK_N(n);
     if (!v || !vh || !d_chunk_stats || chunk <= 0) return VC3_ERR_ARG;
     const int64_t nchunks = (n + chunk - 1) / chunk;
@@ -1049,7 +1067,7 @@ int vc3_error_stats(const float* v, const float* vh, int64_t n, int32_t normalis
     Moments* part = nullptr;
     int st = cuda_status(cudaMallocAsync((void**)&part, sizeof(Moments) * slices * nchunks, s));
     if (st) return st;
-    k_err_partial<<<dim3(slices, (unsigned)nchunks), kStatThreads, 0, s>>>(v, vh, n, normalised,
+    k_err_partial<<<dim3(slices, (unsigned)nchunks), kStatThreads, 0, s>>>(v, vh, n, kind,
                                                                           chunk, slices, part);
     k_err_final<<<grid_for(nchunks), kThreads, 0, s>>>(part, nchunks, slices, d_chunk_stats);
     st = launch_status();

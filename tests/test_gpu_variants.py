@@ -178,3 +178,26 @@ def test_anisotropy_and_precision_comparison_match_reference(golden, vc3b, cuda)
         ("unit_sphere", "single", "single"), ("unit_sphere", "single", "double")]
     arr = np.array([[r["mean"], r["max"], r["stddev"], r["count"]] for r in got])
     np.testing.assert_allclose(arr, ref, rtol=1e-6)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("metric,kind", [("l2", 0), ("angular", 2), ("relative_magnitude", 3)])
+def test_error_metrics_match_cpu_restatement(vc3b, cuda, metric, kind):
+    """K6 per-chunk moments of every error metric against the numpy
+    restatement (oracle/vc3_stats.py) on the same vectors; ragged chunks,
+    zero vectors included."""
+    import torch
+    import vc3_stats
+
+    from paper_2003_02633_b200 import analysis
+
+    v = analysis.sample(analysis.SampleDomain("cube", 300_001, 17))
+    v[::1000] = 0.0
+    tv = torch.from_numpy(v).cuda()
+    vh = vc3b.decompress(vc3b.compress(tv))
+    got = analysis.chunk_moments(tv, vh, False, 1 << 16, metric).cpu().numpy()
+    want = vc3_stats.chunk_moments(v, vh.cpu().numpy(), kind, 1 << 16)
+    assert np.array_equal(got[:, 0], want[:, 0])
+    np.testing.assert_allclose(got[:, 1:], want[:, 1:], rtol=1e-9)
+    st = analysis.error_study(analysis.SampleDomain("unit_sphere", 200_000, 3), metric=metric)
+    assert st.count == 200_000 and st.mean > 0 and st.max >= st.mean

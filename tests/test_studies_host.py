@@ -36,3 +36,27 @@ def test_criterion_4b_joint_coding_exact():
     joint = analysis.joint_encode(nt.ravel(), nph.ravel(), cfg)
     nt2, nph2 = analysis.joint_decode(joint, cfg)
     assert joint.max() < 256 and np.array_equal(nt2, nt.ravel()) and np.array_equal(nph2, nph.ravel())
+
+
+def test_error_metric_restatement_properties():
+    """oracle/vc3_stats.py (the CPU restatement of the K6 metrics)."""
+    import numpy as np
+    import vc3_stats as st
+
+    v = np.array([[1, 0, 0], [0, 2, 0], [3, 4, 0], [0, 0, 0]], np.float32)
+    same = st.errors(v, v, st.ANGULAR)
+    assert np.array_equal(same, np.zeros(4))
+    assert np.allclose(st.errors(v, 2 * v, st.ANGULAR), 0.0)
+    orth = np.array([[0, 1, 0], [1, 0, 0], [-4, 3, 0], [1, 1, 1]], np.float32)
+    assert np.allclose(st.errors(v, orth, st.ANGULAR)[:3], np.pi / 2)
+    assert np.allclose(st.errors(v, 2 * v, st.REL_MAGNITUDE), [1, 1, 1, 0])
+    assert np.allclose(st.errors(v, 2 * v, st.L2), [1, 2, 5, 0])
+    assert np.allclose(st.errors(v, 2 * v, st.L2_NORMALISED), [1, 1, 1, 0])
+    m = st.chunk_moments(np.tile(v, (5, 1)), np.tile(2 * v, (5, 1)), st.L2, 8)
+    assert m.shape == (3, 4) and m[:, 0].tolist() == [8, 8, 4]
+
+
+def test_error_metric_names():
+    with pytest.raises(ValueError):
+        analysis._kind(False, "cosine")
+    assert analysis._kind(True, "l2") == 1 and analysis._kind(True, "angular") == 2
