@@ -443,3 +443,22 @@ def test_lsrk_step_graph_matches_eager(vc3b, cuda):
     torch.cuda.synchronize()
     assert torch.equal(qa, qb) and torch.equal(dqa, dqb)
     assert not torch.equal(qa, q0)
+
+
+@pytest.mark.gpu
+def test_host_entry_points_multi_chunk(vc3b, cuda):
+    """vc3_*_host stream 2^23-vector chunks over three CUDA streams: several
+    chunks plus a ragged tail equal the device-buffer results word for word."""
+    n = 3 * (1 << 22) + 777
+    g = torch.Generator(device=cuda).manual_seed(11)
+    va = torch.rand((n, 3), device=cuda, generator=g).mul_(2).sub_(1)
+    vb = torch.rand((n, 3), device=cuda, generator=g).mul_(2).sub_(1)
+    lay, pol = vc3b.DEFAULT_LAYOUT, vc3b.ALL_SINGLE_POLICY
+    a_dev, b_dev = vc3b.compress(va, lay, pol), vc3b.compress(vb, lay, pol)
+    a_host = vc3b.compress(va.cpu().numpy(), lay, pol)            # vc3_compress_host
+    assert np.array_equal(a_host, a_dev.cpu().numpy())
+    c_host = vc3b.add_compressed(a_host, b_dev.cpu().numpy(), lay, pol)  # vc3_add_compressed_host
+    assert np.array_equal(c_host, vc3b.add_compressed(a_dev, b_dev, lay, pol).cpu().numpy())
+    d_host = vc3b.decompress(c_host, lay)                            # vc3_decompress_host
+    d_dev = vc3b.decompress(torch.from_numpy(c_host.view(np.int64)).to(cuda).view(torch.uint64), lay)
+    assert np.array_equal(d_host.view(np.uint32), d_dev.cpu().numpy().view(np.uint32))
