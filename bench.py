@@ -500,7 +500,9 @@ def run_gpu(args, world, rank, local):
     del out_v
 
     # e2e: public host-array API, pinned host buffers, copies inside the region
-    e2e_n = min(n, N_PER_GPU)  # pinned host staging bounded at one 2^28 shard
+    # pinned host staging: one 2^28 shard (6 GiB) at N = 1; a quarter of that
+    # per rank under torchrun so eight ranks pin 12 GiB, not 48
+    e2e_n = min(n, N_PER_GPU if world == 1 else N_PER_GPU // 4)
     ha = torch.empty(e2e_n, dtype=torch.uint64, pin_memory=True)
     hb = torch.empty(e2e_n, dtype=torch.uint64, pin_memory=True)
     ha.copy_(a[:e2e_n])
