@@ -40,6 +40,10 @@ using namespace vc3::rt;
 
 namespace {
 
+#ifndef VC3_FR_HEX_REG
+#define VC3_FR_HEX_REG 1
+#endif
+
 constexpr int kRows = 256;             // elements per tile: two UMMA M = 128 halves
 constexpr int kHalf = 128;
 constexpr int kPts = 8;                // solution points per K stage
@@ -591,10 +595,14 @@ struct HexOp {
     float m[6][6];
 };
 
-template <int K>
-__global__ void __launch_bounds__(128) k_fr_hex_f32(const float* __restrict__ raw, float* __restrict__ out,
-                                                    int64_t n_elem, int n_vars, int64_t ld, HexOp op) {
+template <int K, bool COMP, class LAY>
+__global__ void __launch_bounds__(128, 3) k_fr_hex_reg(const float* __restrict__ raw, float* __restrict__ out,
+                                                    int64_t n_elem, int n_vars, int64_t ld, HexOp op,
+                                                    const unsigned long long* __restrict__ words = nullptr,
+                                                    Params Pin = Params{}) {
     constexpr int N1 = K + 1, NS = N1 * N1 * N1, PF = 8;
+    Params P = Pin;
+    if (COMP) LAY::apply(P);
     const int c = blockIdx.y;
     const int64_t plane = (int64_t)n_vars * ld;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_elem;
@@ -604,19 +612,33 @@ __global__ void __launch_bounds__(128) k_fr_hex_f32(const float* __restrict__ ra
 #pragma unroll
         for (int k = 0; k < NS; ++k) acc[k] = 0.0f;
         float3 pf[PF];  // the next PF points' fluxes are in flight
+        unsigned long long pw[PF];
 #pragma unroll
         for (int q = 0; q < PF; ++q) {
-            const float* p = raw + 3 * (base + q * plane);
-            pf[q] = make_float3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
+            if (COMP) {
+                pw[q] = __ldg(words + base + q * plane);
+            } else {
+                const float* p = raw + 3 * (base + q * plane);
+                pf[q] = make_float3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
+            }
         }
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
-            const float x = pf[j % PF].x, y = pf[j % PF].y, z = pf[j % PF].z;
-            if (j + PF < NS) {
-                const float* p = raw + 3 * (base + (j + PF) * plane);
-                pf[j % PF] = make_float3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
+            float x, y, z;
+            if (COMP) {
+                decode_f32<LAY>(pw[j % PF], P, x, y, z);
+            } else {
+                x = pf[j % PF].x; y = pf[j % PF].y; z = pf[j % PF].z;
             }
-            const int jx = j % N1, jy = (j / N1) % N1, jz = j / (N1 * N1);
+            if (j + PF < NS) {
+                if (COMP) {
+                    pw[j % PF] = __ldg(words + base + (j + PF) * plane);
+                } else {
+                    const float* p = raw + 3 * (base + (j + PF) * plane);
+                    pf[j % PF] = make_float3(__ldg(p), __ldg(p + 1), __ldg(p + 2));
+                }
+            }
+        const int jx = j % N1, jy = (j / N1) % N1, jz = j / (N1 * N1);
 #pragma unroll
             for (int a = 0; a < N1; ++a) {
                 acc[a + N1 * jy + N1 * N1 * jz] = __fmaf_rn(op.m[a][jx], x, acc[a + N1 * jy + N1 * N1 * jz]);
@@ -661,11 +683,13 @@ __global__ void __launch_bounds__(kHexThreads, 4) k_fr_hex_staged(
         const int c = (int)(t / blocks_per_var);
         const int64_t i = (t - (int64_t)c * blocks_per_var) * kHexE + lane;
         const bool ok = t < ntiles && i < n_elem;
-        const unsigned long long* wp = words + (int64_t)c * ld + i;
+        const unsigned long long* wp = words + (int64_t)c * ld + i + warp * plane;
+        const int64_t wstep = NW * plane;
 #pragma unroll
         for (int r = 0; r < NJ; ++r) {
             const int j = warp + NW * r;
-            w[r] = (ok && j < NS) ? __ldg(wp + j * plane) : 0ull;
+            w[r] = (ok && j < NS) ? __ldg(wp) : 0ull;
+            wp += wstep;
         }
     };
     load_tile(blockIdx.x);
@@ -693,12 +717,16 @@ __global__ void __launch_bounds__(kHexThreads, 4) k_fr_hex_staged(
         float* op_out = out + (int64_t)c * ld + i;
         for (int L = warp; L < N1 * N1; L += NW) {
             const int ky = L % N1, kz = L / N1;
+            // row bases: every inner offset below is a compile-time constant
+            const float* xl = xs + (N1 * L) * kHexE + lane;
+            const float* yl = xs + (NS + N1 * N1 * kz) * kHexE + lane;
+            const float* zl = xs + (2 * NS + N1 * ky) * kHexE + lane;
             float my[N1], mz[N1], xv[N1], acc[N1];
 #pragma unroll
             for (int a = 0; a < N1; ++a) {
                 my[a] = op.m[ky][a];
                 mz[a] = op.m[kz][a];
-                xv[a] = xs[(0 * NS + a + N1 * L) * kHexE + lane];
+                xv[a] = xl[a * kHexE];
             }
 #pragma unroll
             for (int kx = 0; kx < N1; ++kx) {
@@ -706,16 +734,18 @@ __global__ void __launch_bounds__(kHexThreads, 4) k_fr_hex_staged(
 #pragma unroll
                 for (int a = 0; a < N1; ++a) t = __fmaf_rn(op.m[kx][a], xv[a], t);
 #pragma unroll
-                for (int a = 0; a < N1; ++a)
-                    t = __fmaf_rn(my[a], xs[(1 * NS + kx + N1 * a + N1 * N1 * kz) * kHexE + lane], t);
+                for (int a = 0; a < N1; ++a) t = __fmaf_rn(my[a], yl[(kx + N1 * a) * kHexE], t);
 #pragma unroll
-                for (int a = 0; a < N1; ++a)
-                    t = __fmaf_rn(mz[a], xs[(2 * NS + kx + N1 * ky + N1 * N1 * a) * kHexE + lane], t);
+                for (int a = 0; a < N1; ++a) t = __fmaf_rn(mz[a], zl[(kx + N1 * N1 * a) * kHexE], t);
                 acc[kx] = t;
             }
             if (live) {
+                float* o = op_out + (int64_t)(N1 * L) * plane;
 #pragma unroll
-                for (int kx = 0; kx < N1; ++kx) op_out[(kx + N1 * L) * plane] = acc[kx];
+                for (int kx = 0; kx < N1; ++kx) {
+                    o[0] = acc[kx];
+                    o += plane;
+                }
             }
         }
         __syncthreads();
@@ -733,7 +763,14 @@ int hex_launch_k(const unsigned long long* words, const float* raw, float* out, 
     if (blocks > cap) blocks = cap;
     const dim3 grid((unsigned)blocks, (unsigned)n_vars);
     if (raw) {
-        k_fr_hex_f32<K><<<grid, 128, 0, s>>>(raw, out, n_elem, n_vars, ld, op);
+        k_fr_hex_reg<K, false, RuntimeLayout><<<grid, 128, 0, s>>>(raw, out, n_elem, n_vars, ld, op);
+    } else if (VC3_FR_HEX_REG && K != 3) {
+        // register-resident accumulators with the MUFU decode in the point
+        // loop; at k = 3 the compiler's schedule spills, the staged kernel wins
+        if (is_default_layout(*layout))
+            k_fr_hex_reg<K, true, DefaultLayout><<<grid, 128, 0, s>>>(nullptr, out, n_elem, n_vars, ld, op, words, P);
+        else
+            k_fr_hex_reg<K, true, RuntimeLayout><<<grid, 128, 0, s>>>(nullptr, out, n_elem, n_vars, ld, op, words, P);
     } else {
         constexpr int NS = (K + 1) * (K + 1) * (K + 1);
         smem += (size_t)3 * NS * kHexE * sizeof(float);
