@@ -388,6 +388,31 @@ def run_secondary(args, vc3b, lib, dev, stream, n):
                              "measured dense bf16 rate (MEASURED_PEAKS.json)"}}
     del F, words, div, op
     torch.cuda.empty_cache()
+
+    # sum-factorised kernels across degrees (same ~1.3 GB of words each):
+    # where the compressed fluxes overtake the fp32 ones
+    per_k = {}
+    for kk in (1, 2, 3, 4):
+        nsk = (kk + 1) ** 3
+        ne = (n_el * 125) // nsk
+        Fk = torch.rand((nsk, n_vars, ne, 3), device=dev, generator=gen).mul_(2).sub_(1)
+        wk = vc3b.compress(Fk.reshape(-1, 3), lay, vc3b.ALL_SINGLE_POLICY).reshape(nsk, n_vars, ne)
+        dk = torch.empty((nsk, n_vars, ne), dtype=torch.float32, device=dev)
+        mk = np.ascontiguousarray(fr.lagrange_derivative_matrix(fr.gauss_legendre_nodes(kk)),
+                                  dtype=np.float32)
+        hck = lambda: lib.vc3_fr_divergence_hex(wk.data_ptr(), mk.ctypes.data, kk, dk.data_ptr(), ne,
+                                                n_vars, ne, cl, stream.cuda_stream)
+        hfk = lambda: lib.vc3_fr_divergence_hex_f32(Fk.data_ptr(), mk.ctypes.data, kk, dk.data_ptr(),
+                                                    ne, n_vars, ne, stream.cuda_stream)
+        hck(); hfk()
+        torch.cuda.synchronize()
+        tck, tfk = time_region(hck, steps, stream, torch), time_region(hfk, steps, stream, torch)
+        rk_ = ne * n_vars
+        per_k[str(kk)] = {"compressed": rk_ / (tck * 1e-3) / 1e9, "fp32": rk_ / (tfk * 1e-3) / 1e9,
+                          "speedup": tfk / tck}
+        del Fk, wk, dk
+    out["C6_fr_divergence"]["sum_factorised"]["per_degree_g_elem_eq_s"] = per_k
+    torch.cuda.empty_cache()
     return out
 
 
