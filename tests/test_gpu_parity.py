@@ -462,3 +462,26 @@ def test_host_entry_points_multi_chunk(vc3b, cuda):
     d_host = vc3b.decompress(c_host, lay)                            # vc3_decompress_host
     d_dev = vc3b.decompress(torch.from_numpy(c_host.view(np.int64)).to(cuda).view(torch.uint64), lay)
     assert np.array_equal(d_host.view(np.uint32), d_dev.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_empty_inputs_everywhere(vc3b, cuda, tmp_path):
+    """n = 0 through every entry point, host and device arrays."""
+    from paper_2003_02633_b200 import ops, stream
+
+    lay, pol = vc3b.DEFAULT_LAYOUT, vc3b.ALL_SINGLE_POLICY
+    ev = torch.empty((0, 3), dtype=torch.float32, device=cuda)
+    ew = torch.empty(0, dtype=torch.uint64, device=cuda)
+    assert vc3b.compress(ev).numel() == 0 and vc3b.decompress(ew).shape == (0, 3)
+    assert vc3b.compress(np.empty((0, 3), np.float32)).shape == (0,)
+    assert vc3b.decompress(np.empty(0, np.uint64)).shape == (0, 3)
+    assert vc3b.add_compressed(ew, ew).numel() == 0
+    assert vc3b.add_compressed(np.empty(0, np.uint64), np.empty(0, np.uint64)).shape == (0,)
+    assert vc3b.add_raw(np.empty((0, 3), np.float32), np.empty((0, 3), np.float32)).shape == (0, 3)
+    assert ops.axpy(2.0, ew, ew).numel() == 0
+    q, dq = ops.rk_stage(0.5, 0.5, 0.1, ew.clone(), ew.clone(), ew)
+    assert q.numel() == 0 and dq.numel() == 0
+    assert vc3b.magnitude_event_counts(ev) == (0, 0)
+    stream.write_stream(tmp_path / "e.vc3", ew)
+    words, lay2 = stream.read_stream(tmp_path / "e.vc3")
+    assert words.size == 0 and lay2 == lay and (tmp_path / "e.vc3").stat().st_size == 20
