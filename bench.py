@@ -155,7 +155,8 @@ def dist_setup(args):
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = "gloo" if args.impl == "reference" else "nccl"
+        backend = ("gloo" if args.impl == "reference" or os.environ.get("VC3_BENCH_SHARE_GPU") == "1"
+                   else "nccl")
         if backend == "nccl":
             import torch
 
@@ -422,7 +423,10 @@ def run_gpu(args, world, rank, local):
     import paper_2003_02633_b200 as vc3b
     from paper_2003_02633_b200 import _native
 
-    dev = torch.device("cuda", local)
+    # VC3_BENCH_SHARE_GPU=1: functional check of the multi-rank path on a
+    # one-GPU box (ranks share cuda:0 over gloo; its timings are not results)
+    share = os.environ.get("VC3_BENCH_SHARE_GPU") == "1"
+    dev = torch.device("cuda", local % torch.cuda.device_count() if share else local)
     torch.cuda.set_device(dev)
     _native.load()
     lay, pol = vc3b.DEFAULT_LAYOUT, vc3b.ALL_SINGLE_POLICY
@@ -449,7 +453,8 @@ def run_gpu(args, world, rank, local):
             return x
         import torch.distributed as dist
 
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        on_gpu = dist.get_backend() == "nccl"
+        t = torch.tensor([x], dtype=torch.float64, device=dev if on_gpu else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -477,7 +482,7 @@ def run_gpu(args, world, rank, local):
     def timed(label_steps):
         barrier()
         torch.cuda.synchronize()
-        with ClockSampler(local) as clk:
+        with ClockSampler(dev.index) as clk:
             ms = time_region(step_add, label_steps, stream, torch)
         torch.cuda.synchronize()
         barrier()
@@ -538,7 +543,7 @@ def run_gpu(args, world, rank, local):
 
     def step_e2e():
         rc2 = lib.vc3_add_compressed_host(na.ctypes.data, nb.ctypes.data, hc.ctypes.data, e2e_n,
-                                          cl, pol.mask, local)
+                                          cl, pol.mask, dev.index)
         _native.check(rc2, "add_compressed_host")
 
     step_e2e()
