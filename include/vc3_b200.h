@@ -76,6 +76,12 @@ int vc3_compress(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout
 int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout,
                    void* stream);
 
+/* vc3_compress and the magnitude events of the same vectors in one pass
+ * (codec.py:241-262): d_events[0] += flushed, d_events[1] +=
+ * saturated (device uint64[2], zeroed by the caller). */
+int vc3_compress_events(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout,
+                        uint32_t policy, int32_t* d_nonfinite, uint64_t* d_events, void* stream);
+
 /* bench.add_compressed (bench.py:41-69) -> add_compressed_kernel (_kernels.py:348-359):
  * c = compress(decompress(a) + decompress(b)) fused, nothing uncompressed
  * touches memory.  The reference's default policy here is ALL_SINGLE. */

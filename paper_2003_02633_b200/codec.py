@@ -111,6 +111,34 @@ def compress(vectors, layout=DEFAULT_LAYOUT, policy=DEFAULT_POLICY):
     return out
 
 
+def compress_with_events(vectors, layout=DEFAULT_LAYOUT, policy=DEFAULT_POLICY):
+    """``(compress(vectors), magnitude_event_counts(vectors))`` in one pass over
+    the input (the event counters fused into the compress kernel).
+    Host arrays are uploaded once; the words come back to the host."""
+    layout, policy = as_layout(layout), as_policy(policy)
+    lib = _native.load()
+    host = not _dev.is_device(vectors)
+    if host:
+        hv = _host_vectors(vectors)
+        if hv.shape[0] == 0:
+            return np.empty(0, dtype=np.uint64), (0, 0)
+        v = _dev.upload(hv)
+    else:
+        v = _device_vectors(vectors)
+    n = v.shape[0]
+    out = torch.empty(n, dtype=torch.uint64, device=v.device)
+    bad = torch.zeros(1, dtype=torch.int32, device=v.device)
+    ev = torch.zeros(2, dtype=torch.int64, device=v.device)
+    _native.check(lib.vc3_compress_events(v.data_ptr(), out.data_ptr(), n, _native.c_layout(layout),
+                                          policy.mask, bad.data_ptr(), ev.data_ptr(),
+                                          _dev.stream_of(v)), "compress_events")
+    nbad = int(bad.item())
+    if nbad:
+        raise NonFiniteInput(_nonfinite_message(nbad))
+    counts = ev.cpu().tolist()
+    return (_dev.download(out) if host else out), (int(counts[0]), int(counts[1]))
+
+
 def decompress(words, layout=DEFAULT_LAYOUT):
     """Reconstruct (n, 3) float32 vectors from packed words (codec.py:205-228).
 

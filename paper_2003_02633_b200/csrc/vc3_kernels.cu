@@ -314,14 +314,17 @@ __device__ __forceinline__ void load_table(double2* sm, const double2* __restric
 // ===================== kernels ==============================================
 
 // K1 compress: 4 vectors (48 B in, 32 B out) per thread per step.
-template <unsigned POLICY, bool NARROW, class LAY>
+// EV: also count the magnitude events (K8, codec.py:241-262) in the same pass.
+template <unsigned POLICY, bool NARROW, class LAY, bool EV = false>
 __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_compress(const float* __restrict__ xyz,
                                                        unsigned long long* __restrict__ out,
                                                        int64_t n, Params Pin, bool vec,
-                                                       int32_t* __restrict__ nonfinite) {
+                                                       int32_t* __restrict__ nonfinite,
+                                                       unsigned long long* __restrict__ events = nullptr) {
     Params P = Pin;
     LAY::apply(P);
     int bad = 0;
+    unsigned ev[2] = {0u, 0u};
     const int64_t groups = vec ? n / 4 : 0;
     // (shared-memory staging of this input was measured slower: the kernel
     // is issue-bound, so the 16-byte strided loads stay; the next step's
@@ -339,18 +342,22 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_compress(con
         }
         bad += !finite3(a.x, a.y, a.z) + !finite3(a.w, b.x, b.y) + !finite3(b.z, b.w, c.x) +
                !finite3(c.y, c.z, c.w);
-        const unsigned long long w0 = compress_one<POLICY, kFma, NARROW>(a.x, a.y, a.z, P);
-        const unsigned long long w1 = compress_one<POLICY, kFma, NARROW>(a.w, b.x, b.y, P);
-        const unsigned long long w2 = compress_one<POLICY, kFma, NARROW>(b.z, b.w, c.x, P);
-        const unsigned long long w3 = compress_one<POLICY, kFma, NARROW>(c.y, c.z, c.w, P);
+        const unsigned long long w0 = compress_one<POLICY, kFma, NARROW, EV>(a.x, a.y, a.z, P, ev);
+        const unsigned long long w1 = compress_one<POLICY, kFma, NARROW, EV>(a.w, b.x, b.y, P, ev);
+        const unsigned long long w2 = compress_one<POLICY, kFma, NARROW, EV>(b.z, b.w, c.x, P, ev);
+        const unsigned long long w3 = compress_one<POLICY, kFma, NARROW, EV>(c.y, c.z, c.w, P, ev);
         st_u4(out + 4 * g, w0, w1, w2, w3);
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         const float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
         bad += !finite3(x, y, z);
-        out[i] = compress_one<POLICY, kFma, NARROW>(x, y, z, P);
+        out[i] = compress_one<POLICY, kFma, NARROW, EV>(x, y, z, P, ev);
     }
     if (bad && nonfinite) atomicAdd(nonfinite, bad);
+    if (EV) {
+        if (ev[0]) atomicAdd(events, (unsigned long long)ev[0]);
+        if (ev[1]) atomicAdd(events + 1, (unsigned long long)ev[1]);
+    }
 }
 
 // K2 decompress: 4 words (32 B in, 48 B out) per thread per step.
@@ -788,15 +795,24 @@ int by_policy(uint32_t pol, A... args) {
 template <unsigned POL>
 struct RunCompress {
     static int run(const float* x, uint64_t* w, int64_t n, const Params& P, bool def, int32_t* nf,
-                   cudaStream_t s) {
+                   unsigned long long* ev, cudaStream_t s) {
         const bool vec = aligned16(x) && aligned32(w);
         const unsigned grid = grid_for(vec ? (n + 3) / 4 : n, VC3_COMPRESS_CTAS_PER_SM);
-        if (def)
-            k_compress<POL, true, DefaultLayout><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
-        else if (P.t <= 29 && P.p <= 29)
-            k_compress<POL, true, RuntimeLayout><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
-        else
-            k_compress<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(x, (unsigned long long*)w, n, P, vec, nf);
+        auto W = (unsigned long long*)w;
+        if (ev) {
+            if (def)
+                k_compress<POL, true, DefaultLayout, true><<<grid, kThreads, 0, s>>>(x, W, n, P, vec, nf, ev);
+            else if (P.t <= 29 && P.p <= 29)
+                k_compress<POL, true, RuntimeLayout, true><<<grid, kThreads, 0, s>>>(x, W, n, P, vec, nf, ev);
+            else
+                k_compress<POL, false, RuntimeLayout, true><<<grid, kThreads, 0, s>>>(x, W, n, P, vec, nf, ev);
+        } else if (def) {
+            k_compress<POL, true, DefaultLayout><<<grid, kThreads, 0, s>>>(x, W, n, P, vec, nf);
+        } else if (P.t <= 29 && P.p <= 29) {
+            k_compress<POL, true, RuntimeLayout><<<grid, kThreads, 0, s>>>(x, W, n, P, vec, nf);
+        } else {
+            k_compress<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(x, W, n, P, vec, nf);
+        }
         return launch_status();
     }
 };
@@ -898,7 +914,19 @@ int vc3_compress(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout
     VC3_CHECK_N(n);
     if (!xyz || !words) return VC3_ERR_ARG;
     return by_policy<RunCompress>(policy, xyz, words, n, make_params(layout),
-                                  is_default_layout(layout), d_nonfinite, (cudaStream_t)stream);
+                                  is_default_layout(layout), d_nonfinite,
+                                  (unsigned long long*)nullptr, (cudaStream_t)stream);
+}
+
+int vc3_compress_events(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout,
+                        uint32_t policy, int32_t* d_nonfinite, uint64_t* d_events, void* stream) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    if (policy > 7u) return VC3_ERR_ARG;
+    VC3_CHECK_N(n);
+    if (!xyz || !words || !d_events) return VC3_ERR_ARG;
+    return by_policy<RunCompress>(policy, xyz, words, n, make_params(layout),
+                                  is_default_layout(layout), d_nonfinite,
+                                  (unsigned long long*)d_events, (cudaStream_t)stream);
 }
 
 int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout, void* stream) {

@@ -485,3 +485,24 @@ def test_empty_inputs_everywhere(vc3b, cuda, tmp_path):
     stream.write_stream(tmp_path / "e.vc3", ew)
     words, lay2 = stream.read_stream(tmp_path / "e.vc3")
     assert words.size == 0 and lay2 == lay and (tmp_path / "e.vc3").stat().st_size == 20
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lname,code", [("17_18", "SSS"), ("17_18", "SDS"), ("base_16_16", "DDD"),
+                                        ("wide_10_25", "SSS")])
+def test_compress_with_events_fused(golden, vc3b, cuda, lname, code):
+    """K8: the fused pass gives the compress words and the event counts of the
+    separate kernels (and the reference's counts on its fixtures)."""
+    from paper_2003_02633_b200 import codec
+
+    lay, pol = layout_by_name(lname), policy_by_code(code)
+    for key in ("vec_mixed", "vec_edge"):
+        v = golden[key]
+        words, ev = codec.compress_with_events(v, lay, pol)
+        assert np.array_equal(words, vc3b.compress(v, lay, pol))
+        assert ev == vc3b.magnitude_event_counts(v, lay)
+        if lname == "17_18":
+            assert ev == tuple(golden["mag_events_" + key[4:]])
+    tv = torch.from_numpy(golden["vec_mixed"]).to(cuda)
+    dw, dev_ev = codec.compress_with_events(tv, lay, pol)
+    assert dw.is_cuda and dev_ev == vc3b.magnitude_event_counts(golden["vec_mixed"], lay)
