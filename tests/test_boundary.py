@@ -104,3 +104,24 @@ def test_python_api_surface_matches_reference():
                 if mine[: len(params)] != params:
                     problems.append(f"{mod_name}.{name}{tuple(params)} vs ours {tuple(mine)}")
     assert not problems, problems
+
+
+def test_alias_as_vc3(monkeypatch):
+    """``alias_as_vc3`` makes reference-style imports resolve to this package."""
+    import importlib
+    import sys
+
+    for k in [k for k in sys.modules if k == "vc3" or k.startswith("vc3.")]:
+        monkeypatch.delitem(sys.modules, k)
+    import paper_2003_02633_b200 as pkg
+
+    pkg.alias_as_vc3()
+    try:
+        vc3 = importlib.import_module("vc3")
+        from vc3 import analysis, codec, stream  # noqa: F401
+
+        assert vc3 is pkg and codec.compress is pkg.compress
+        assert stream.HEADER_SIZE == 20 and hasattr(analysis, "error_study")
+    finally:
+        for k in [k for k in sys.modules if k == "vc3" or k.startswith("vc3.")]:
+            del sys.modules[k]
