@@ -11,22 +11,30 @@
 // against 1,500 B of compressed input and output — beyond the FP32 CUDA-core
 // rate at HBM speed — so the contraction runs on tcgen05:
 //
-//  * one CTA per tile of 128 elements of one equation; 8 decode warps, one
+//  * persistent CTAs (one per SM), tiles of 256 elements of one equation as
+//    two UMMA M = 128 halves; 16 decode warps, 4 epilogue warps, one
 //    operator-load warp (cp.async.bulk of the pre-split operator slice from
-//    L2), one MMA warp (a single elected thread issues tcgen05.mma);
+//    L2), one flux-row warp (cp.async.bulk of each stage's 8 rows into a
+//    shared-memory ring) and one MMA warp (a single thread issues
+//    tcgen05.mma);
 //  * K is walked in stages of 8 solution points (24 k-values): the decode
 //    warps write the stage's A slice straight into shared memory in the
 //    canonical no-swizzle K-major UMMA layout (8-row x 16-byte core
-//    matrices), the MMA warp accumulates into TMEM (128 lanes x Npad fp32
-//    columns), stages ring through NST buffers guarded by mbarriers;
+//    matrices), the MMA warp accumulates into TMEM (two halves x npad fp32
+//    columns, double-buffered across tiles), stages ring through mbarriers;
+//  * the operand decode is float32 (MUFU sin/cos, decode_f32): the GEMM's
+//    own rounding is larger than its error;
 //  * fp32 accuracy on TF32 tensor cores by operand splitting (3xTF32):
 //    a = a_hi + a_lo, b = b_hi + b_lo with a_hi the top 19 bits, and
 //    a*b ~ a_hi*b_hi + a_hi*b_lo + a_lo*b_hi (relative error ~2^-21);
-//  * epilogue: tcgen05.ld of the accumulator (lane = element, column = k),
-//    coalesced 128-byte stores per output point.
+//  * epilogue warps: tcgen05.ld of the accumulator (lane = element, column =
+//    point), coalesced 128-byte stores per output point, overlapping the
+//    next tile's mainloop.
 //
 // The uncompressed baseline (float32 [j][c][i][3] fluxes) runs the same
-// kernel with plain loads in place of the decode.
+// kernel with plain loads in place of the decode.  For tensor-product
+// hexahedra the sum-factorised kernels at the end of this file apply the
+// 1D derivative matrix per direction on the CUDA cores instead.
 #include <cuda_runtime.h>
 
 #include <cstdint>
