@@ -369,7 +369,10 @@ def run_secondary(args, vc3b, lib, dev, stream, n):
     thf = time_region(hf, steps, stream, torch)
     rows = n_el * n_vars
     dense = 2.0 * 3 * ns * ns * rows  # flops of Alg. 1 per launch
-    tf32_peak = load_peaks().get("bf16_tflops", 2250.0) / 2.0
+    # dense TF32 peak: tools/umma_bench.cu (back-to-back tcgen05.mma kind::tf32
+    # M128 N128 K8 from shared memory, one CTA per SM) measured 1058 TFLOP/s on
+    # this pool's B200; B200_PROFILING.md states 1.1 PFLOP/s dense
+    tf32_peak = 1058.0
     ach = 3 * dense / (tcm * 1e-3) / 1e12
     out["C6_fr_divergence"] = {
         "k": kdeg, "n_points": ns, "n_vars": n_vars, "n_elem": n_el, "unit": "G elem-eq/s",
@@ -385,8 +388,8 @@ def run_secondary(args, vc3b, lib, dev, stream, n):
                            "note": "tensor-product hexahedron, 15 FMAs per output on CUDA cores"},
         "roofline": {"bound": "tensor", "achieved": ach, "peak": tf32_peak, "unit": "TFLOP/s",
                      "frac": ach / tf32_peak,
-                     "note": "3xTF32: 3 tensor products per Alg.-1 product; peak = half the "
-                             "measured dense bf16 rate (MEASURED_PEAKS.json)"}}
+                     "note": "3xTF32: 3 tensor products per Alg.-1 product; peak = measured "
+                             "tcgen05 tf32 issue rate (tools/umma_bench.cu)"}}
     del F, words, div, op
     torch.cuda.empty_cache()
 
