@@ -479,6 +479,7 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin) 
         if (lane == 0) {
             const uint32_t idesc = idesc_tf32(kHalf, a.npad);
             const int bsl = b_slice_bytes(a.npad);
+            const uint64_t desc0 = smem_desc(stages, 128, 256);
             int b = 0, use = 0, lt = 0;
             for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++lt) {
                 const int ab = nacc == 2 ? (lt & 1) : 0;
@@ -488,17 +489,21 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin) 
                 for (int s = 0; s < a.nst; ++s) {
                     mbar_wait(&full[b], use & 1);
                     tc_fence_after();
-                    const unsigned char* st = stages + (size_t)b * sbytes;
-                    const unsigned char* bs = st + 12 * kASliceBytes;
+                    // descriptors = slot base descriptor + (byte offset >> 4): one
+                    // add each (the MMA thread shares its scheduler with decode
+                    // warps, so its instruction count per MMA matters)
+                    const uint64_t sd = desc0 + (uint64_t)(((uint32_t)b * (uint32_t)sbytes) >> 4);
+                    const uint64_t bd = sd + (uint64_t)((12 * kASliceBytes) >> 4);
+                    const uint32_t acc0 = tmem + (uint32_t)(ab * 2 * a.npad);
 #pragma unroll
                     for (int d = 0; d < 3; ++d) {
-                        const uint64_t bhi = smem_desc(bs + d * bsl, 128, 256);
-                        const uint64_t blo = smem_desc(bs + (3 + d) * bsl, 128, 256);
+                        const uint64_t bhi = bd + (uint64_t)((uint32_t)(d * bsl) >> 4);
+                        const uint64_t blo = bd + (uint64_t)((uint32_t)((3 + d) * bsl) >> 4);
 #pragma unroll
                         for (int m = 0; m < 2; ++m) {
-                            const uint32_t acc = tmem + (uint32_t)((ab * 2 + m) * a.npad);
-                            const uint64_t ahi = smem_desc(st + a_slice(0, m, d), 128, 256);
-                            const uint64_t alo = smem_desc(st + a_slice(1, m, d), 128, 256);
+                            const uint32_t acc = acc0 + (uint32_t)(m * a.npad);
+                            const uint64_t ahi = sd + (uint64_t)(a_slice(0, m, d) >> 4);
+                            const uint64_t alo = sd + (uint64_t)(a_slice(1, m, d) >> 4);
                             mma_tf32(acc, alo, bhi, idesc, (s | d) != 0);
                             mma_tf32(acc, ahi, blo, idesc, 1);
                             mma_tf32(acc, ahi, bhi, idesc, 1);
