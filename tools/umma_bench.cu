@@ -15,7 +15,7 @@ __device__ __forceinline__ uint32_t idesc(int m, int n) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
-template <int N>
+template <int N, bool TS>
 __global__ void __launch_bounds__(128, 1) k_bench(int iters, unsigned long long* cycles) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint32_t tslot;
@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(128, 1) k_bench(int iters, unsigned long long*
         asm volatile("fence.mbarrier_init.release.cluster;");
     }
     if (threadIdx.x < 32) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tslot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("fence.proxy.async.shared::cta;");
@@ -40,9 +40,14 @@ __global__ void __launch_bounds__(128, 1) k_bench(int iters, unsigned long long*
         const uint32_t id = idesc(128, N);
         const long long t0 = clock64();
         for (int i = 0; i < iters; ++i) {
-            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
-                         "l"(a), "l"(b), "r"(id), "r"(i));
+            if (TS)  // A from TMEM (columns 256.. of the allocation)
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem),
+                             "r"(tmem + 256u), "l"(b), "r"(id), "r"(i));
+            else
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+                             "l"(a), "l"(b), "r"(id), "r"(i));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
         uint32_t done = 0;
@@ -53,21 +58,21 @@ __global__ void __launch_bounds__(128, 1) k_bench(int iters, unsigned long long*
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int N>
+template <int N, bool TS>
 void run(int sms) {
     const int iters = 20000;
     unsigned long long* d;
     cudaMalloc(&d, sms * 8);
     const size_t smem = (size_t)(128 + N) * 8 * 4 * 2 + 1024;
-    cudaFuncSetAttribute(k_bench<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_bench<N><<<sms, 128, smem>>>(100, d);
+    cudaFuncSetAttribute(k_bench<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_bench<N, TS><<<sms, 128, smem>>>(100, d);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    k_bench<N><<<sms, 128, smem>>>(iters, d);
+    k_bench<N, TS><<<sms, 128, smem>>>(iters, d);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -75,7 +80,7 @@ void run(int sms) {
     unsigned long long c;
     cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
     const double flops = 2.0 * 128 * N * 8 * (double)iters * sms;
-    printf("N=%3d: %.1f TFLOP/s tf32 dense (%.1f cycles per MMA on SM0) err=%s\n", N, flops / (ms * 1e-3) / 1e12,
+    printf("%s N=%3d: %.1f TFLOP/s tf32 dense (%.1f cycles per MMA on SM0) err=%s\n", TS ? "A:tmem" : "A:smem", N, flops / (ms * 1e-3) / 1e12,
            (double)c / iters, cudaGetErrorString(cudaGetLastError()));
     cudaFree(d);
 }
@@ -83,8 +88,10 @@ void run(int sms) {
 int main() {
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    run<64>(sms);
-    run<128>(sms);
-    run<256>(sms);
+    run<64, false>(sms);
+    run<128, false>(sms);
+    run<256, false>(sms);
+    run<128, true>(sms);
+    run<256, true>(sms);
     return 0;
 }
