@@ -17,8 +17,14 @@
 
 namespace {
 
-constexpr int kStreams = 3;
-constexpr int64_t kChunk = int64_t(1) << 23;  // vectors per chunk (64 MiB of words)
+#ifndef VC3_HOST_STREAMS
+#define VC3_HOST_STREAMS 3
+#endif
+#ifndef VC3_HOST_CHUNK_LOG2
+#define VC3_HOST_CHUNK_LOG2 23
+#endif
+constexpr int kStreams = VC3_HOST_STREAMS;
+constexpr int64_t kChunk = int64_t(1) << VC3_HOST_CHUNK_LOG2;  // vectors per chunk (2^23: 64 MiB of words)
 
 struct DeviceCtx {
     cudaMemPool_t pool = nullptr;
