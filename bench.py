@@ -607,7 +607,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=N_PER_GPU, help="vectors per GPU")
+    ap.add_argument("--n", "--vectors", dest="n", type=int, default=N_PER_GPU,
+                    help="vectors per GPU (--vectors under torchrun: its parser claims --n)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: --n vectors per GPU (C2); strong: --total split over GPUs (C5)")
     ap.add_argument("--total", type=int, default=1 << 31, help="global vectors for --scaling strong")

@@ -42,3 +42,29 @@ def test_reference_arm_under_torchrun_rank0_only():
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_gpu_arm_multirank_code_path_on_one_gpu():
+    """Functional check of the N > 1 path of bench.py (torchrun, two ranks,
+    barrier + max-over-ranks, rank-0 line) on a one-GPU box: the ranks share
+    cuda:0 over gloo (VC3_BENCH_SHARE_GPU); the timing is not a result."""
+    import os
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, VC3_BENCH_SHARE_GPU="1")
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                          "--master-port", str(port), str(ROOT / "bench.py"), "--gpus", "2",
+                          "--steps", "3", "--warmup", "3", "--vectors", str(1 << 22), "--no-secondary"],
+                         capture_output=True, text=True, check=True, timeout=600, env=env)
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["global_vectors"] == 2 << 22
