@@ -178,6 +178,46 @@ int get_table(const Params& P, const double2** out) {
     return VC3_OK;
 }
 
+// The reference's own decode tables (_kernels.py:252-273): glibc sin/cos of
+// th = _PI*(2n/ntmax - 1) and ph = _PI*n/npmax, exact pole; 6 MB at the
+// default layout, device-resident, read only for the rare boundary cases of
+// the bit-identical decompress.
+std::map<TableKey, double2*> g_full;
+
+int get_full_table(const Params& P, const double2** out) {
+    *out = nullptr;
+    if (!P.table_mode) return VC3_OK;
+    const TableKey key{current_device(), P.t, P.p};
+    std::lock_guard<std::mutex> lock(g_tab_mu);
+    auto it = g_full.find(key);
+    if (it != g_full.end()) {
+        *out = it->second;
+        return VC3_OK;
+    }
+    std::vector<double2> h((size_t)(P.ntmax + 1 + P.npmax + 1));
+    const volatile double pi = kPi;
+    for (long long n = 0; n <= P.ntmax; ++n) {
+        const double th = pi * (2.0 * (double)n / (double)P.ntmax - 1.0);
+        h[(size_t)n] = make_double2(std::sin(th), std::cos(th));
+    }
+    for (long long n = 0; n <= P.npmax; ++n) {
+        const double ph = pi * (double)n / (double)P.npmax;
+        h[(size_t)(P.ntmax + 1 + n)] = make_double2(std::sin(ph), std::cos(ph));
+    }
+    h[(size_t)(P.ntmax + 1 + P.npmax)] = make_double2(0.0, -1.0);
+    double2* d = nullptr;
+    int st = cuda_status(cudaMalloc((void**)&d, h.size() * sizeof(double2)));
+    if (st) return st;
+    st = cuda_status(cudaMemcpy(d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    if (st) {
+        cudaFree(d);
+        return st;
+    }
+    g_full[key] = d;
+    *out = d;
+    return VC3_OK;
+}
+
 size_t table_smem(const Params& P) { return P.table_mode ? (size_t)P.tab_n * sizeof(double2) : 0; }
 
 // Opt a kernel into more than 48 KB of dynamic shared memory (the default
@@ -207,6 +247,11 @@ constexpr int kThreads = 256;
 // >= 4 resident CTAs per SM (<= 64 registers) give the best fused-add issue rate
 #ifndef VC3_FUSED_MIN_BLOCKS
 #define VC3_FUSED_MIN_BLOCKS 4
+#endif
+// decompress bit-identical to the reference's libm decode (boundary cases
+// re-evaluated from the reference's own tables; vc3_device.cuh)
+#ifndef VC3_DECOMP_EXACT
+#define VC3_DECOMP_EXACT 1
 #endif
 #ifndef VC3_DECOMP_STAGE
 #define VC3_DECOMP_STAGE 1
@@ -365,7 +410,8 @@ template <bool TABLE, class LAY>
 __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_decompress(const unsigned long long* __restrict__ w,
                                                          float* __restrict__ xyz, int64_t n,
                                                          Params Pin, bool vec,
-                                                         const double2* __restrict__ gtab) {
+                                                         const double2* __restrict__ gtab,
+                                                         const double2* __restrict__ full) {
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
@@ -391,10 +437,10 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
         const int64_t gn = g + gstride();
         if (gn < groups) wn = ld_stream_u4(w + 4 * gn);
         float o[12];
-        decompress_one<TABLE>(u.x, P, tt, tp, o[0], o[1], o[2]);
-        decompress_one<TABLE>(u.y, P, tt, tp, o[3], o[4], o[5]);
-        decompress_one<TABLE>(u.z, P, tt, tp, o[6], o[7], o[8]);
-        decompress_one<TABLE>(u.w, P, tt, tp, o[9], o[10], o[11]);
+        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.x, P, tt, tp, o[0], o[1], o[2], full);
+        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.y, P, tt, tp, o[3], o[4], o[5], full);
+        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.z, P, tt, tp, o[6], o[7], o[8], full);
+        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.w, P, tt, tp, o[9], o[10], o[11], full);
 #if VC3_DECOMP_STAGE
         stage[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
         stage[3 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
@@ -422,7 +468,7 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float x, y, z;
-        decompress_one<TABLE>(w[i], P, tt, tp, x, y, z);
+        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(w[i], P, tt, tp, x, y, z, full);
         xyz[3 * i] = x;
         xyz[3 * i + 1] = y;
         xyz[3 * i + 2] = z;
@@ -937,6 +983,11 @@ int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layo
     const double2* tab = nullptr;
     int st = get_table(P, &tab);
     if (st) return st;
+    const double2* full = nullptr;
+    if (VC3_DECOMP_EXACT) {
+        st = get_full_table(P, &full);
+        if (st) return st;
+    }
     auto W = (const unsigned long long*)words;
     const bool vec = aligned32(words) && aligned16(xyz);
     const int64_t items = vec ? (n + 3) / 4 : n;
@@ -952,11 +1003,11 @@ int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layo
     st = ensure_smem(fn, smem);
     if (st) return st;
     if (is_default_layout(layout))
-        k_decompress<true, DefaultLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab);
+        k_decompress<true, DefaultLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab, full);
     else if (P.table_mode)
-        k_decompress<true, RuntimeLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab);
+        k_decompress<true, RuntimeLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab, full);
     else
-        k_decompress<false, RuntimeLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab);
+        k_decompress<false, RuntimeLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab, full);
     return launch_status();
 }
 
