@@ -250,6 +250,9 @@ constexpr int kThreads = 256;
 #endif
 // decompress bit-identical to the reference's libm decode (boundary cases
 // re-evaluated from the reference's own tables; vc3_device.cuh)
+#ifndef VC3_FUSED_EXACT
+#define VC3_FUSED_EXACT 0
+#endif
 #ifndef VC3_DECOMP_EXACT
 #define VC3_DECOMP_EXACT 1
 #endif
@@ -479,10 +482,10 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
 template <unsigned POLICY, bool TABLE>
 __device__ __forceinline__ unsigned long long add_one(unsigned long long a, unsigned long long b,
                                                       const Params& P, const double2* tt,
-                                                      const double2* tp) {
+                                                      const double2* tp, const double2* full = nullptr) {
     float x1, y1, z1, x2, y2, z2;
-    decompress_one<TABLE, true>(a, P, tt, tp, x1, y1, z1);
-    decompress_one<TABLE, true>(b, P, tt, tp, x2, y2, z2);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT>(a, P, tt, tp, x1, y1, z1, full);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT>(b, P, tt, tp, x2, y2, z2, full);
     return compress_one<POLICY, kFma, TABLE>(__fadd_rn(x1, x2), __fadd_rn(y1, y2), __fadd_rn(z1, z2), P);
 }
 
@@ -491,7 +494,8 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_add(const un
                                                   const unsigned long long* __restrict__ b,
                                                   unsigned long long* __restrict__ c, int64_t n,
                                                   Params Pin, bool vec,
-                                                  const double2* __restrict__ gtab) {
+                                                  const double2* __restrict__ gtab,
+                                                  const double2* __restrict__ full) {
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
@@ -504,14 +508,14 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_add(const un
     const int64_t groups = vec ? n / kV : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
         const u64x4 u = ld_stream_u4(a + kV * g), v = ld_stream_u4(b + kV * g);
-        const unsigned long long c0 = add_one<POLICY, TABLE>(u.x, v.x, P, tt, tp);
-        const unsigned long long c1 = add_one<POLICY, TABLE>(u.y, v.y, P, tt, tp);
-        const unsigned long long c2 = add_one<POLICY, TABLE>(u.z, v.z, P, tt, tp);
-        const unsigned long long c3 = add_one<POLICY, TABLE>(u.w, v.w, P, tt, tp);
+        const unsigned long long c0 = add_one<POLICY, TABLE>(u.x, v.x, P, tt, tp, full);
+        const unsigned long long c1 = add_one<POLICY, TABLE>(u.y, v.y, P, tt, tp, full);
+        const unsigned long long c2 = add_one<POLICY, TABLE>(u.z, v.z, P, tt, tp, full);
+        const unsigned long long c3 = add_one<POLICY, TABLE>(u.w, v.w, P, tt, tp, full);
         st_u4(c + kV * g, c0, c1, c2, c3);
     }
     for (int64_t i = groups * kV + gtid(); i < n; i += gstride())
-        c[i] = add_one<POLICY, TABLE>(a[i], b[i], P, tt, tp);
+        c[i] = add_one<POLICY, TABLE>(a[i], b[i], P, tt, tp, full);
 }
 
 // K5 uncompressed baseline: flat float32 add (_kernels.py:341-345)
@@ -871,12 +875,17 @@ struct RunAdd {
         auto C = (unsigned long long*)c;
         const bool vec = aligned32(a) && aligned32(b) && aligned32(c);
         const unsigned grid = grid_for(vec ? (n + 3) / 4 : n, VC3_ADD_CTAS_PER_SM);
+        const double2* full = nullptr;
+        if (VC3_FUSED_EXACT) {
+            const int st = get_full_table(P, &full);
+            if (st) return st;
+        }
         if (def)
-            VC3_LAUNCH_TABLE((k_add<POL, true, DefaultLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_add<POL, true, DefaultLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab, full);
         else if (P.table_mode)
-            VC3_LAUNCH_TABLE((k_add<POL, true, RuntimeLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_add<POL, true, RuntimeLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab, full);
         else
-            k_add<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(A, B, C, n, P, vec, tab);
+            k_add<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(A, B, C, n, P, vec, tab, full);
         return launch_status();
     }
 };
