@@ -72,7 +72,10 @@ int vc3_compress(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout
                  uint32_t policy, int32_t* d_nonfinite, void* stream);
 
 /* codec.decompress (codec.py:205-228) -> decompress_kernel_tab/_direct
- * (_kernels.py:293-331).  words: uint64 [n]; xyz: float32 [n][3]. */
+ * (_kernels.py:293-331).  words: uint64 [n]; xyz: float32 [n][3].
+ * Bit-identical to the reference's decode (its libm sin/cos tables): the
+ * first call for a layout builds a 49 KB shared-memory table and the 6 MB
+ * reference table on the device (call once before graph capture). */
 int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout,
                    void* stream);
 
