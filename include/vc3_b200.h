@@ -71,6 +71,13 @@ int vc3_validate_layout(vc3_layout layout);
 int vc3_compress(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout,
                  uint32_t policy, int32_t* d_nonfinite, void* stream);
 
+/* The bound, relative to the magnitude, by which the fast table decode's
+ * components can differ from the reference's doubles (measured over every
+ * table index against the reference's tables); components within it of a
+ * float32 rounding boundary are re-evaluated exactly.  0 for layouts decoded
+ * without tables.  Synchronous; builds the tables on first use. */
+int vc3_decode_tolerance(vc3_layout layout, double* tol);
+
 /* codec.decompress (codec.py:205-228) -> decompress_kernel_tab/_direct
  * (_kernels.py:293-331).  words: uint64 [n]; xyz: float32 [n][3].
  * Bit-identical to the reference's decode (its libm sin/cos tables): the

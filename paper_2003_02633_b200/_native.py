@@ -49,6 +49,7 @@ SIGNATURES = {
     "vc3_validate_layout": ([Layout], ctypes.c_int),
     "vc3_compress": ([_p, _p, _i64, Layout, _u32, _p, _p], ctypes.c_int),
     "vc3_decompress": ([_p, _p, _i64, Layout, _p], ctypes.c_int),
+    "vc3_decode_tolerance": ([Layout, _p], ctypes.c_int),
     "vc3_compress_events": ([_p, _p, _i64, Layout, _u32, _p, _p, _p], ctypes.c_int),
     "vc3_add_compressed": ([_p, _p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
     "vc3_add_raw": ([_p, _p, _p, _i64, _p], ctypes.c_int),

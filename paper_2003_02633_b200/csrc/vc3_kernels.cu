@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -184,9 +185,45 @@ int get_table(const Params& P, const double2** out) {
 // the bit-identical decompress.
 std::map<TableKey, double2*> g_full;
 
+// Largest |fast table sin/cos - reference sin/cos| over every theta index
+// (err[0]) and every phi index (err[1]), as decompress_one indexes the table.
+__global__ void k_table_err(const double2* __restrict__ tab, const double2* __restrict__ full,
+                            Params P, unsigned long long* err) {
+    const long long nT = P.ntmax + 1, nP = P.npmax + 1;
+    double et = 0.0, ep = 0.0;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nT + nP;
+         i += (long long)gridDim.x * blockDim.x) {
+        double s, c;
+        const double2 A = full[i];
+        if (i < nT) {
+            const int nt = (int)i;
+            const bool endp = nt == (int)P.ntmax;
+            sincos_tab(tab, endp ? P.t_n - 1 : nt >> P.t_shift, endp ? 0 : nt & ((1 << P.t_shift) - 1),
+                       P.t_delta, s, c);
+            et = fmax(et, fmax(fabs(s - A.x), fabs(c - A.y)));
+        } else {
+            const int nph = (int)(i - nT);
+            const bool pole = nph == (int)P.npmax;
+            sincos_tab(tab + P.p_base, pole ? P.p_n - 1 : nph >> P.p_shift,
+                       pole ? 0 : nph & ((1 << P.p_shift) - 1), P.p_delta, s, c);
+            ep = fmax(ep, fmax(fabs(s - A.x), fabs(c - A.y)));
+        }
+    }
+    atomicMax(err, (unsigned long long)__double_as_longlong(et));
+    atomicMax(err + 1, (unsigned long long)__double_as_longlong(ep));
+}
+
+// Decode tolerance (relative to r): a decoded component fl(fl(r*c')*s') vs
+// the reference's fl(fl(r*c)*s) with |c - c'| <= et, |s - s'| <= ep differs
+// by at most r*(et + ep + et*ep + 4u(1 + et)(1 + ep)), u = 2^-53; the
+// boundary test's own d +- e roundings move its ends by <= r*2^-53 more.
+double decode_tolerance(double et, double ep) { return (et + ep) * (1.0 + 0x1p-20) + 0x1p-49; }
+
 int get_full_table(const Params& P, const double2** out) {
     *out = nullptr;
     if (!P.table_mode) return VC3_OK;
+    const double2* seed = nullptr;
+    if (const int st0 = get_table(P, &seed)) return st0;
     const TableKey key{current_device(), P.t, P.p};
     std::lock_guard<std::mutex> lock(g_tab_mu);
     auto it = g_full.find(key);
@@ -194,7 +231,8 @@ int get_full_table(const Params& P, const double2** out) {
         *out = it->second;
         return VC3_OK;
     }
-    std::vector<double2> h((size_t)(P.ntmax + 1 + P.npmax + 1));
+    // [theta: ntmax + 1][phi: npmax + 1][tolerance]
+    std::vector<double2> h((size_t)(P.ntmax + 1 + P.npmax + 1 + 1));
     const volatile double pi = kPi;
     for (long long n = 0; n <= P.ntmax; ++n) {
         const double th = pi * (2.0 * (double)n / (double)P.ntmax - 1.0);
@@ -206,9 +244,24 @@ int get_full_table(const Params& P, const double2** out) {
     }
     h[(size_t)(P.ntmax + 1 + P.npmax)] = make_double2(0.0, -1.0);
     double2* d = nullptr;
-    int st = cuda_status(cudaMalloc((void**)&d, h.size() * sizeof(double2)));
+    int st = cuda_status(cudaMalloc((void**)&d, h.size() * sizeof(double2) + 16));
     if (st) return st;
+    unsigned long long* err = (unsigned long long*)(d + h.size());
     st = cuda_status(cudaMemcpy(d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    if (!st) st = cuda_status(cudaMemset(err, 0, 16));
+    if (!st) {
+        k_table_err<<<2 * 148, 256>>>(seed, d, P, err);
+        st = cuda_status(cudaGetLastError());
+    }
+    unsigned long long e2[2] = {0, 0};
+    if (!st) st = cuda_status(cudaMemcpy(e2, err, 16, cudaMemcpyDeviceToHost));
+    if (!st) {
+        double et, ep;
+        std::memcpy(&et, &e2[0], 8);
+        std::memcpy(&ep, &e2[1], 8);
+        h.back() = make_double2(decode_tolerance(et, ep), 0.0);
+        st = cuda_status(cudaMemcpy(d + h.size() - 1, &h.back(), sizeof(double2), cudaMemcpyHostToDevice));
+    }
     if (st) {
         cudaFree(d);
         return st;
@@ -251,7 +304,7 @@ constexpr int kThreads = 256;
 // decompress bit-identical to the reference's libm decode (boundary cases
 // re-evaluated from the reference's own tables; vc3_device.cuh)
 #ifndef VC3_FUSED_EXACT
-#define VC3_FUSED_EXACT 0
+#define VC3_FUSED_EXACT 1
 #endif
 #ifndef VC3_DECOMP_EXACT
 #define VC3_DECOMP_EXACT 1
@@ -349,6 +402,12 @@ __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * block
 
 // Copy the decode table into shared memory (once per CTA; grids are capped
 // at a few CTAs per SM, so the copy is amortised over the whole stream).
+// the decode's boundary tolerance (relative to the magnitude), stored after
+// the reference's tables by get_full_table
+__device__ __forceinline__ double exact_tol(const double2* __restrict__ full, const Params& P) {
+    return full ? __ldg(full + (P.ntmax + 1) + (P.npmax + 1)).x : 0.0;
+}
+
 template <bool TABLE>
 __device__ __forceinline__ void load_table(double2* sm, const double2* __restrict__ g,
                                            const Params& P) {
@@ -421,6 +480,7 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
+    const double tol = exact_tol(full, P);
     const int64_t groups = vec ? n / 4 : 0;
 #if VC3_DECOMP_STAGE
     // per-warp shared staging of the array-of-structs output: each lane's 48 B
@@ -440,10 +500,10 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
         const int64_t gn = g + gstride();
         if (gn < groups) wn = ld_stream_u4(w + 4 * gn);
         float o[12];
-        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.x, P, tt, tp, o[0], o[1], o[2], full);
-        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.y, P, tt, tp, o[3], o[4], o[5], full);
-        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.z, P, tt, tp, o[6], o[7], o[8], full);
-        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.w, P, tt, tp, o[9], o[10], o[11], full);
+        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.x, P, tt, tp, o[0], o[1], o[2], full, tol);
+        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.y, P, tt, tp, o[3], o[4], o[5], full, tol);
+        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.z, P, tt, tp, o[6], o[7], o[8], full, tol);
+        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.w, P, tt, tp, o[9], o[10], o[11], full, tol);
 #if VC3_DECOMP_STAGE
         stage[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
         stage[3 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
@@ -471,7 +531,7 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float x, y, z;
-        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(w[i], P, tt, tp, x, y, z, full);
+        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(w[i], P, tt, tp, x, y, z, full, tol);
         xyz[3 * i] = x;
         xyz[3 * i + 1] = y;
         xyz[3 * i + 2] = z;
@@ -482,10 +542,11 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
 template <unsigned POLICY, bool TABLE>
 __device__ __forceinline__ unsigned long long add_one(unsigned long long a, unsigned long long b,
                                                       const Params& P, const double2* tt,
-                                                      const double2* tp, const double2* full = nullptr) {
+                                                      const double2* tp, const double2* full,
+                                                      double tol) {
     float x1, y1, z1, x2, y2, z2;
-    decompress_one<TABLE, true, VC3_FUSED_EXACT>(a, P, tt, tp, x1, y1, z1, full);
-    decompress_one<TABLE, true, VC3_FUSED_EXACT>(b, P, tt, tp, x2, y2, z2, full);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT>(a, P, tt, tp, x1, y1, z1, full, tol);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT>(b, P, tt, tp, x2, y2, z2, full, tol);
     return compress_one<POLICY, kFma, TABLE>(__fadd_rn(x1, x2), __fadd_rn(y1, y2), __fadd_rn(z1, z2), P);
 }
 
@@ -502,20 +563,21 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_add(const un
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
+    const double tol = exact_tol(full, P);
     // four independent vectors per thread step give the scheduler ILP across
     // the long FP64 chains; words move with sm_100 256-bit accesses
     constexpr int kV = 4;  // one 32-byte load per operand and one 32-byte store per step
     const int64_t groups = vec ? n / kV : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
         const u64x4 u = ld_stream_u4(a + kV * g), v = ld_stream_u4(b + kV * g);
-        const unsigned long long c0 = add_one<POLICY, TABLE>(u.x, v.x, P, tt, tp, full);
-        const unsigned long long c1 = add_one<POLICY, TABLE>(u.y, v.y, P, tt, tp, full);
-        const unsigned long long c2 = add_one<POLICY, TABLE>(u.z, v.z, P, tt, tp, full);
-        const unsigned long long c3 = add_one<POLICY, TABLE>(u.w, v.w, P, tt, tp, full);
+        const unsigned long long c0 = add_one<POLICY, TABLE>(u.x, v.x, P, tt, tp, full, tol);
+        const unsigned long long c1 = add_one<POLICY, TABLE>(u.y, v.y, P, tt, tp, full, tol);
+        const unsigned long long c2 = add_one<POLICY, TABLE>(u.z, v.z, P, tt, tp, full, tol);
+        const unsigned long long c3 = add_one<POLICY, TABLE>(u.w, v.w, P, tt, tp, full, tol);
         st_u4(c + kV * g, c0, c1, c2, c3);
     }
     for (int64_t i = groups * kV + gtid(); i < n; i += gstride())
-        c[i] = add_one<POLICY, TABLE>(a[i], b[i], P, tt, tp, full);
+        c[i] = add_one<POLICY, TABLE>(a[i], b[i], P, tt, tp, full, tol);
 }
 
 // K5 uncompressed baseline: flat float32 add (_kernels.py:341-345)
@@ -563,10 +625,11 @@ __global__ void __launch_bounds__(kThreads) k_rk_f32(float ca, float cb, float d
 template <unsigned POLICY, bool TABLE>
 __device__ __forceinline__ unsigned long long axpy_one(float al, unsigned long long x,
                                                        unsigned long long y, const Params& P,
-                                                       const double2* tt, const double2* tp) {
+                                                       const double2* tt, const double2* tp,
+                                                       const double2* full, double tol) {
     float x1, y1, z1, x2, y2, z2;
-    decompress_one<TABLE, true>(x, P, tt, tp, x1, y1, z1);
-    decompress_one<TABLE, true>(y, P, tt, tp, x2, y2, z2);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT>(x, P, tt, tp, x1, y1, z1, full, tol);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT>(y, P, tt, tp, x2, y2, z2, full, tol);
     return compress_one<POLICY, kFma, TABLE>(__fadd_rn(__fmul_rn(al, x1), x2),
                                       __fadd_rn(__fmul_rn(al, y1), y2),
                                       __fadd_rn(__fmul_rn(al, z1), z2), P);
@@ -576,33 +639,36 @@ template <unsigned POLICY, bool TABLE, class LAY>
 __global__ void __launch_bounds__(kThreads) k_axpy(float al, const unsigned long long* __restrict__ x,
                                                    const unsigned long long* y,
                                                    unsigned long long* yo, int64_t n, Params Pin,
-                                                   bool vec, const double2* __restrict__ gtab) {
+                                                   bool vec, const double2* __restrict__ gtab,
+                                                   const double2* __restrict__ full) {
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
+    const double tol = exact_tol(full, P);
     const int64_t pairs = vec ? n / 2 : 0;
     for (int64_t g = gtid(); g < pairs; g += gstride()) {
         const ulonglong2 u = ld_stream_u2(x + 2 * g);
         const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(y + 2 * g);  // may alias yo
-        st_u2(yo + 2 * g, axpy_one<POLICY, TABLE>(al, u.x, v.x, P, tt, tp),
-              axpy_one<POLICY, TABLE>(al, u.y, v.y, P, tt, tp));
+        st_u2(yo + 2 * g, axpy_one<POLICY, TABLE>(al, u.x, v.x, P, tt, tp, full, tol),
+              axpy_one<POLICY, TABLE>(al, u.y, v.y, P, tt, tp, full, tol));
     }
     for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride())
-        yo[i] = axpy_one<POLICY, TABLE>(al, x[i], y[i], P, tt, tp);
+        yo[i] = axpy_one<POLICY, TABLE>(al, x[i], y[i], P, tt, tp, full, tol);
 }
 
 // K4b low-storage RK stage: dq' = a*dq + dt*R ; q' = q + b*dq'
 template <unsigned POLICY, bool TABLE>
 __device__ __forceinline__ void rk_one(float ca, float cb, float dt, unsigned long long& q,
                                        unsigned long long& dq, unsigned long long r,
-                                       const Params& P, const double2* tt, const double2* tp) {
+                                       const Params& P, const double2* tt, const double2* tp,
+                                       const double2* full, double tol) {
     float q0, q1, q2, d0, d1, d2, r0, r1, r2;
-    decompress_one<TABLE, true>(q, P, tt, tp, q0, q1, q2);
-    decompress_one<TABLE, true>(dq, P, tt, tp, d0, d1, d2);
-    decompress_one<TABLE, true>(r, P, tt, tp, r0, r1, r2);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT>(q, P, tt, tp, q0, q1, q2, full, tol);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT>(dq, P, tt, tp, d0, d1, d2, full, tol);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT>(r, P, tt, tp, r0, r1, r2, full, tol);
     d0 = __fadd_rn(__fmul_rn(ca, d0), __fmul_rn(dt, r0));
     d1 = __fadd_rn(__fmul_rn(ca, d1), __fmul_rn(dt, r1));
     d2 = __fadd_rn(__fmul_rn(ca, d2), __fmul_rn(dt, r2));
@@ -619,26 +685,28 @@ __global__ void __launch_bounds__(kThreads) k_rk(float ca, float cb, float dt,
                                                  unsigned long long* __restrict__ dq,
                                                  const unsigned long long* __restrict__ R,
                                                  int64_t n, Params Pin, bool vec,
-                                                 const double2* __restrict__ gtab) {
+                                                 const double2* __restrict__ gtab,
+                                                 const double2* __restrict__ full) {
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
+    const double tol = exact_tol(full, P);
     const int64_t pairs = vec ? n / 2 : 0;
     for (int64_t g = gtid(); g < pairs; g += gstride()) {
         ulonglong2 u = *reinterpret_cast<const ulonglong2*>(q + 2 * g);
         ulonglong2 v = *reinterpret_cast<const ulonglong2*>(dq + 2 * g);
         const ulonglong2 r = ld_stream_u2(R + 2 * g);
-        rk_one<POLICY, TABLE>(ca, cb, dt, u.x, v.x, r.x, P, tt, tp);
-        rk_one<POLICY, TABLE>(ca, cb, dt, u.y, v.y, r.y, P, tt, tp);
+        rk_one<POLICY, TABLE>(ca, cb, dt, u.x, v.x, r.x, P, tt, tp, full, tol);
+        rk_one<POLICY, TABLE>(ca, cb, dt, u.y, v.y, r.y, P, tt, tp, full, tol);
         st_u2(q + 2 * g, u.x, u.y);
         st_u2(dq + 2 * g, v.x, v.y);
     }
     for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride()) {
         unsigned long long qq = q[i], dd = dq[i];
-        rk_one<POLICY, TABLE>(ca, cb, dt, qq, dd, R[i], P, tt, tp);
+        rk_one<POLICY, TABLE>(ca, cb, dt, qq, dd, R[i], P, tt, tp, full, tol);
         q[i] = qq;
         dq[i] = dd;
     }
@@ -867,6 +935,12 @@ struct RunCompress {
     }
 };
 
+// the reference's decode tables for the fused kernels' exact redo
+int fused_full_table(const Params& P, const double2** full) {
+    *full = nullptr;
+    return (VC3_FUSED_EXACT && P.table_mode) ? get_full_table(P, full) : 0;
+}
+
 template <unsigned POL>
 struct RunAdd {
     static int run(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t n, const Params& P,
@@ -876,10 +950,7 @@ struct RunAdd {
         const bool vec = aligned32(a) && aligned32(b) && aligned32(c);
         const unsigned grid = grid_for(vec ? (n + 3) / 4 : n, VC3_ADD_CTAS_PER_SM);
         const double2* full = nullptr;
-        if (VC3_FUSED_EXACT) {
-            const int st = get_full_table(P, &full);
-            if (st) return st;
-        }
+        if (const int st = fused_full_table(P, &full)) return st;
         if (def)
             VC3_LAUNCH_TABLE((k_add<POL, true, DefaultLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab, full);
         else if (P.table_mode)
@@ -898,12 +969,14 @@ struct RunAxpy {
         auto O = (unsigned long long*)yo;
         const bool vec = aligned16(x) && aligned16(y) && aligned16(yo);
         const unsigned grid = grid_for(vec ? (n + 1) / 2 : n, VC3_ADD_CTAS_PER_SM);
+        const double2* full = nullptr;
+        if (const int st = fused_full_table(P, &full)) return st;
         if (def)
-            VC3_LAUNCH_TABLE((k_axpy<POL, true, DefaultLayout>), grid, table_smem(P), s, al, X, Y, O, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_axpy<POL, true, DefaultLayout>), grid, table_smem(P), s, al, X, Y, O, n, P, vec, tab, full);
         else if (P.table_mode)
-            VC3_LAUNCH_TABLE((k_axpy<POL, true, RuntimeLayout>), grid, table_smem(P), s, al, X, Y, O, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_axpy<POL, true, RuntimeLayout>), grid, table_smem(P), s, al, X, Y, O, n, P, vec, tab, full);
         else
-            k_axpy<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(al, X, Y, O, n, P, vec, tab);
+            k_axpy<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(al, X, Y, O, n, P, vec, tab, full);
         return launch_status();
     }
 };
@@ -916,12 +989,14 @@ struct RunRk {
         auto RR = (const unsigned long long*)R;
         const bool vec = aligned16(q) && aligned16(dq) && aligned16(R);
         const unsigned grid = grid_for(vec ? (n + 1) / 2 : n, VC3_ADD_CTAS_PER_SM);
+        const double2* full = nullptr;
+        if (const int st = fused_full_table(P, &full)) return st;
         if (def)
-            VC3_LAUNCH_TABLE((k_rk<POL, true, DefaultLayout>), grid, table_smem(P), s, ca, cb, dt, Q, D, RR, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_rk<POL, true, DefaultLayout>), grid, table_smem(P), s, ca, cb, dt, Q, D, RR, n, P, vec, tab, full);
         else if (P.table_mode)
-            VC3_LAUNCH_TABLE((k_rk<POL, true, RuntimeLayout>), grid, table_smem(P), s, ca, cb, dt, Q, D, RR, n, P, vec, tab);
+            VC3_LAUNCH_TABLE((k_rk<POL, true, RuntimeLayout>), grid, table_smem(P), s, ca, cb, dt, Q, D, RR, n, P, vec, tab, full);
         else
-            k_rk<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab);
+            k_rk<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab, full);
         return launch_status();
     }
 };
@@ -982,6 +1057,21 @@ int vc3_compress_events(const float* xyz, uint64_t* words, int64_t n, vc3_layout
     return by_policy<RunCompress>(policy, xyz, words, n, make_params(layout),
                                   is_default_layout(layout), d_nonfinite,
                                   (unsigned long long*)d_events, (cudaStream_t)stream);
+}
+
+int vc3_decode_tolerance(vc3_layout layout, double* tol) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    if (!tol) return VC3_ERR_ARG;
+    const Params P = make_params(layout);
+    *tol = 0.0;
+    const double2* full = nullptr;
+    int st = get_full_table(P, &full);
+    if (st || !full) return st;
+    double2 last;
+    st = cuda_status(cudaMemcpy(&last, full + (P.ntmax + 1) + (P.npmax + 1), sizeof(last),
+                                cudaMemcpyDeviceToHost));
+    if (!st) *tol = last.x;
+    return st;
 }
 
 int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout, void* stream) {

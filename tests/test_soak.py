@@ -2,9 +2,9 @@
 oracle on every host core.  Skipped unless VC3_SOAK=<log2 total vectors per
 case> is set (e.g. VC3_SOAK=32); the counts it prints are recorded in
 profiles/r01_soak.json.  All-single policy (the benchmark's): compressed
-words and fused-add words must match bit for bit; the default policy may
-differ only by single-bin ties; decoded components of random words must be
-bit-exact for >= 99.99 % and within 2 ulp for all."""
+words, fused-add words and RK-stage words must match bit for bit; the default
+policy may differ only by single-bin ties; decoded components of random words
+must be bit-exact."""
 
 import json
 import os
@@ -82,14 +82,30 @@ def test_soak(vc3b, oracle, cuda):
         report[kind] = {"compress_all_single_mismatches": mis_sss, "compress_default_ties": ties_sds,
                         "fused_add_mismatches": mis_add}
         report["fused_add_mismatch_details"] = details
-        # compress is bit-exact; a fused-add word may differ only when a decoded
-        # operand differs by 1 ulp from the reference's libm decode, and then by
-        # one bin / one magnitude step
+        # compress and the fused add are bit-exact (the fused decodes take the
+        # reference's tables near a float32 rounding boundary)
         assert mis_sss == 0, report
-        assert mis_add <= 1e-8 * total, report
-        for d_ in details:
-            assert abs(d_["dtheta"]) <= 1 and abs(d_["dphi"]) <= 1 and abs(d_["dfield"]) <= 1, report
+        assert mis_add == 0, report
         assert ties_sds <= 1e-4 * total, report
+    # low-storage RK stage on equator vectors (the ICV field's w = 0: decoded z
+    # ~ -1.2e-5 r, the decode's hardest case for the boundary test), 1/8 of
+    # the vectors: words bit-exact vs the oracle composition
+    g = np.random.Generator(np.random.Philox(key=(SOAK, 7)))
+    mis_rk = 0
+    for _ in range(max(1, total // CHUNK // 8)):
+        v = g.normal(size=(3, CHUNK, 3)).astype(np.float32)
+        v[:, :, 2] = 0.0
+        q, dq, R = (oracle.compress(x, lay, sss, nthreads=nthr) for x in v)
+        tq, tdq, tR = (torch.from_numpy(x.view(np.int64)).to(cuda).view(torch.uint64) for x in (q, dq, R))
+        a, b, dt = np.float32(-0.41789047), np.float32(1.4965424), np.float32(1e-3)
+        vc3b.rk_stage(a, b, dt, tq, tdq, tR, lay, sss)
+        qd, dqd, Rd = (oracle.decompress(x, lay, nthreads=nthr) for x in (q, dq, R))
+        dq_new = a * dqd + dt * Rd
+        q_new = qd + b * dq_new
+        mis_rk += int((tdq.cpu().numpy().view(np.uint64) != oracle.compress(dq_new, lay, sss, nthreads=nthr)).sum())
+        mis_rk += int((tq.cpu().numpy().view(np.uint64) != oracle.compress(q_new, lay, sss, nthreads=nthr)).sum())
+    report["rk_stage_equator"] = {"vectors": max(1, total // CHUNK // 8) * CHUNK, "word_mismatches": mis_rk}
+    assert mis_rk == 0, report
     # decompress of random words
     g = np.random.Generator(np.random.Philox(key=(SOAK, 99)))
     exact = ulp_max = n_words = 0
@@ -108,4 +124,4 @@ def test_soak(vc3b, oracle, cuda):
     report["decompress_random_words"] = {"components": 3 * n_words, "exact": exact, "max_ulp": ulp_max}
     report["seconds"] = round(time.time() - t0, 1)
     print("SOAK", json.dumps(report))
-    assert ulp_max <= 2 and exact >= 0.9999 * 3 * n_words, report
+    assert ulp_max == 0 and exact == 3 * n_words, report
