@@ -303,6 +303,9 @@ constexpr int kThreads = 256;
 #endif
 // decompress bit-identical to the reference's libm decode (boundary cases
 // re-evaluated from the reference's own tables; vc3_device.cuh)
+#ifndef VC3_RK_CELL
+#define VC3_RK_CELL 0  // the RK stage keeps the two-conversion boundary test (ICV field: see DESIGN §9)
+#endif
 #ifndef VC3_FUSED_EXACT
 #define VC3_FUSED_EXACT 1
 #endif
@@ -666,9 +669,9 @@ __device__ __forceinline__ void rk_one(float ca, float cb, float dt, unsigned lo
                                        const Params& P, const double2* tt, const double2* tp,
                                        const double2* full, double tol) {
     float q0, q1, q2, d0, d1, d2, r0, r1, r2;
-    decompress_one<TABLE, true, VC3_FUSED_EXACT>(q, P, tt, tp, q0, q1, q2, full, tol);
-    decompress_one<TABLE, true, VC3_FUSED_EXACT>(dq, P, tt, tp, d0, d1, d2, full, tol);
-    decompress_one<TABLE, true, VC3_FUSED_EXACT>(r, P, tt, tp, r0, r1, r2, full, tol);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT, VC3_RK_CELL>(q, P, tt, tp, q0, q1, q2, full, tol);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT, VC3_RK_CELL>(dq, P, tt, tp, d0, d1, d2, full, tol);
+    decompress_one<TABLE, true, VC3_FUSED_EXACT, VC3_RK_CELL>(r, P, tt, tp, r0, r1, r2, full, tol);
     d0 = __fadd_rn(__fmul_rn(ca, d0), __fmul_rn(dt, r0));
     d1 = __fadd_rn(__fmul_rn(ca, d1), __fmul_rn(dt, r1));
     d2 = __fadd_rn(__fmul_rn(ca, d2), __fmul_rn(dt, r2));
