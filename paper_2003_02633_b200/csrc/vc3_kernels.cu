@@ -407,8 +407,11 @@ __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * block
 // at a few CTAs per SM, so the copy is amortised over the whole stream).
 // the decode's boundary tolerance (relative to the magnitude), stored after
 // the reference's tables by get_full_table
+// CELL: the cell test (needs_exact<true>) takes the doubled tolerance
+template <bool CELL = false>
 __device__ __forceinline__ double exact_tol(const double2* __restrict__ full, const Params& P) {
-    return full ? __ldg(full + (P.ntmax + 1) + (P.npmax + 1)).x : 0.0;
+    const double t = full ? __ldg(full + (P.ntmax + 1) + (P.npmax + 1)).x : 0.0;
+    return CELL ? __dadd_rn(t, t) : t;
 }
 
 template <bool TABLE>
@@ -566,7 +569,7 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_add(const un
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
-    const double tol = exact_tol(full, P);
+    const double tol = exact_tol<VC3_CELL_CHECK>(full, P);
     // four independent vectors per thread step give the scheduler ILP across
     // the long FP64 chains; words move with sm_100 256-bit accesses
     constexpr int kV = 4;  // one 32-byte load per operand and one 32-byte store per step
@@ -650,7 +653,7 @@ __global__ void __launch_bounds__(kThreads) k_axpy(float al, const unsigned long
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
-    const double tol = exact_tol(full, P);
+    const double tol = exact_tol<VC3_CELL_CHECK>(full, P);
     const int64_t pairs = vec ? n / 2 : 0;
     for (int64_t g = gtid(); g < pairs; g += gstride()) {
         const ulonglong2 u = ld_stream_u2(x + 2 * g);
