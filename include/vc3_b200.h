@@ -48,6 +48,19 @@ typedef struct vc3_layout {
 #define VC3_POLICY_ORACLE 0u                                                       /* layout.py:184 */
 #define VC3_POLICY_ALL_SINGLE (VC3_THETA_SINGLE | VC3_PHI_SINGLE | VC3_QUANT_SINGLE) /* layout.py:185 */
 
+/* Numerics mode of the decoding operations (the *_ex entry points).
+ *   VC3_EXACT    bit-identical to the reference: decoded components equal the
+ *                reference's decode of the same word, output words equal the
+ *                reference's (the plain entry points always use this mode);
+ *   VC3_CONTRACT the tolerance of the north-star contract (BASELINE.json): the
+ *                table decode without its exactness test, so a decoded
+ *                component may be one float32 ulp from the reference's and a
+ *                re-compressed word may then move by one bin at a tie.  The
+ *                compress half stays bit-exact for its inputs. */
+#define VC3_EXACT 0u
+#define VC3_CONTRACT 1u
+#define VC3_FLAGS_ALL 1u
+
 typedef enum vc3_status {
     VC3_OK = 0,
     VC3_ERR_LAYOUT = -1,    /* BadLayout (layout.py:47-69)                  */
@@ -85,6 +98,9 @@ int vc3_decode_tolerance(vc3_layout layout, double* tol);
  * reference table on the device (call once before graph capture). */
 int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout,
                    void* stream);
+/* vc3_decompress with a numerics mode (VC3_EXACT / VC3_CONTRACT). */
+int vc3_decompress_ex(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout,
+                      uint32_t flags, void* stream);
 
 /* vc3_compress and the magnitude events of the same vectors in one pass
  * (codec.py:241-262): d_events[0] += flushed, d_events[1] +=
@@ -97,6 +113,9 @@ int vc3_compress_events(const float* xyz, uint64_t* words, int64_t n, vc3_layout
  * touches memory.  The reference's default policy here is ALL_SINGLE. */
 int vc3_add_compressed(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t n,
                        vc3_layout layout, uint32_t policy, void* stream);
+/* vc3_add_compressed with a numerics mode (VC3_EXACT / VC3_CONTRACT). */
+int vc3_add_compressed_ex(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t n,
+                          vc3_layout layout, uint32_t policy, uint32_t flags, void* stream);
 
 /* bench.add_raw (bench.py:30-38) -> add_raw_kernel (_kernels.py:341-345):
  * the uncompressed float32 baseline, c[i] = a[i] + b[i] over n_floats floats. */
@@ -107,6 +126,8 @@ int vc3_add_raw(const float* a, const float* b, float* c, int64_t n_floats, void
  * y_out may alias y (in-place update). */
 int vc3_axpy(float alpha, const uint64_t* x, const uint64_t* y, uint64_t* y_out, int64_t n,
              vc3_layout layout, uint32_t policy, void* stream);
+int vc3_axpy_ex(float alpha, const uint64_t* x, const uint64_t* y, uint64_t* y_out, int64_t n,
+                vc3_layout layout, uint32_t policy, uint32_t flags, void* stream);
 
 /* Low-storage (2N) RK stage on compressed registers (SURVEY §8a R18,
  * PAPER.md:135,336), all three operands stored compressed:
@@ -116,6 +137,8 @@ int vc3_axpy(float alpha, const uint64_t* x, const uint64_t* y, uint64_t* y_out,
  * updated in place (40 B of HBM traffic per vector). */
 int vc3_rk_stage(float a, float b, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
                  int64_t n, vc3_layout layout, uint32_t policy, void* stream);
+int vc3_rk_stage_ex(float a, float b, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
+                    int64_t n, vc3_layout layout, uint32_t policy, uint32_t flags, void* stream);
 
 /* Uncompressed float32 baseline of vc3_rk_stage (60 B of HBM traffic per
  * vector): the same op order on flat float32 arrays of n_floats elements. */

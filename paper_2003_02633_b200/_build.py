@@ -17,8 +17,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 LIB = LIB_DIR / "libvc3_b200.so"
-SOURCES = ["vc3_kernels.cu", "vc3_host.cu", "vc3_variants.cu", "vc3_fr.cu"]
-HEADERS = ["vc3_device.cuh", "vc3_rt.h"]
+SOURCES = ["vc3_kernels.cu", "vc3_fused.cu", "vc3_host.cu", "vc3_variants.cu", "vc3_fr.cu"]
+HEADERS = ["vc3_device.cuh", "vc3_fused.cuh", "vc3_kern_common.cuh", "vc3_rt.h"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NUMERICS = ["-fmad=false", "-ftz=false", "-prec-div=true", "-prec-sqrt=true"]
@@ -39,20 +39,37 @@ def _stale() -> bool:
     return any(d.stat().st_mtime > built for d in deps)
 
 
+def _compile_cmd(src: Path, obj: Path, verbose: bool) -> list[str]:
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", *NUMERICS, "-Xcompiler", "-fPIC",
+           "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    return cmd
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile the shared library if any source is newer than it."""
+    """Compile the shared library if any source is newer than it.
+
+    Each translation unit compiles to its own object in parallel (the fused
+    kernels' template instantiations dominate the build), then one link."""
     if not force and not _stale():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
+    obj_dir = LIB_DIR / "obj"
+    obj_dir.mkdir(exist_ok=True)
+    objs = [obj_dir / (Path(s).stem + ".o") for s in SOURCES]
+    procs = []
+    for src, obj in zip(SOURCES, objs):
+        cmd = _compile_cmd(CSRC / src, obj, verbose)
+        if verbose:
+            print(" ".join(cmd))
+        procs.append((src, subprocess.Popen(cmd)))
+    failed = [src for src, p in procs if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc {' '.join(failed)}")
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", *NUMERICS,
-           "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
-           "-I", str(ROOT / "include"),
-           *(str(CSRC / s) for s in SOURCES), "-o", str(tmp)]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+    subprocess.run([nvcc(), *ARCH, "-shared", "-cudart", "static", *(str(o) for o in objs),
+                    "-o", str(tmp)], check=True)
     os.replace(tmp, LIB)
     return LIB
 

@@ -49,12 +49,16 @@ SIGNATURES = {
     "vc3_validate_layout": ([Layout], ctypes.c_int),
     "vc3_compress": ([_p, _p, _i64, Layout, _u32, _p, _p], ctypes.c_int),
     "vc3_decompress": ([_p, _p, _i64, Layout, _p], ctypes.c_int),
+    "vc3_decompress_ex": ([_p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
     "vc3_decode_tolerance": ([Layout, _p], ctypes.c_int),
     "vc3_compress_events": ([_p, _p, _i64, Layout, _u32, _p, _p, _p], ctypes.c_int),
     "vc3_add_compressed": ([_p, _p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
+    "vc3_add_compressed_ex": ([_p, _p, _p, _i64, Layout, _u32, _u32, _p], ctypes.c_int),
     "vc3_add_raw": ([_p, _p, _p, _i64, _p], ctypes.c_int),
     "vc3_axpy": ([_f32, _p, _p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
+    "vc3_axpy_ex": ([_f32, _p, _p, _p, _i64, Layout, _u32, _u32, _p], ctypes.c_int),
     "vc3_rk_stage": ([_f32, _f32, _f32, _p, _p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
+    "vc3_rk_stage_ex": ([_f32, _f32, _f32, _p, _p, _p, _i64, Layout, _u32, _u32, _p], ctypes.c_int),
     "vc3_rk_stage_f32": ([_f32, _f32, _f32, _p, _p, _p, _i64, _p], ctypes.c_int),
     "vc3_to_spherical": ([_p, _p, _p, _p, _i64, _u32, _p, _p], ctypes.c_int),
     "vc3_quantize_angles": ([_p, _p, _p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
@@ -76,6 +80,10 @@ SIGNATURES = {
     "vc3_compress_host": ([_p, _p, _i64, Layout, _u32, _p, _i32], ctypes.c_int),
     "vc3_decompress_host": ([_p, _p, _i64, Layout, _i32], ctypes.c_int),
 }
+
+# numerics modes of the *_ex entry points (include/vc3_b200.h)
+VC3_EXACT = 0
+VC3_CONTRACT = 1
 
 VC3_OK = 0
 VC3_ERR_LAYOUT = -1

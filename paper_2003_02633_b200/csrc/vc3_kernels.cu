@@ -291,138 +291,10 @@ int ensure_smem(const void* func, size_t bytes) {
 
 }  // namespace rt
 }  // namespace vc3
-using namespace vc3::rt;
+
+#include "vc3_kern_common.cuh"
 
 namespace {
-
-constexpr int kThreads = 256;
-// measured on B200 (tools/occupancy_sweep.py): 4 vectors per thread step and
-// >= 4 resident CTAs per SM (<= 64 registers) give the best fused-add issue rate
-#ifndef VC3_FUSED_MIN_BLOCKS
-#define VC3_FUSED_MIN_BLOCKS 4
-#endif
-// decompress bit-identical to the reference's libm decode (boundary cases
-// re-evaluated from the reference's own tables; vc3_device.cuh)
-#ifndef VC3_RK_CELL
-#define VC3_RK_CELL 0  // the RK stage keeps the two-conversion boundary test (ICV field: see DESIGN §9)
-#endif
-#ifndef VC3_FUSED_EXACT
-#define VC3_FUSED_EXACT 1
-#endif
-#ifndef VC3_DECOMP_EXACT
-#define VC3_DECOMP_EXACT 1
-#endif
-#ifndef VC3_DECOMP_STAGE
-#define VC3_DECOMP_STAGE 1
-#endif
-// grid caps in CTAs per SM for the streaming kernels (grid-stride beyond);
-// more CTAs than resident slots balance the tail across SMs (measured)
-#ifndef VC3_ADD_CTAS_PER_SM
-#define VC3_ADD_CTAS_PER_SM 48
-#endif
-#ifndef VC3_COMPRESS_CTAS_PER_SM
-#define VC3_COMPRESS_CTAS_PER_SM 48
-#endif
-#ifndef VC3_DECOMP_CTAS_PER_SM
-#define VC3_DECOMP_CTAS_PER_SM 4
-#endif
-// decompress CTAs: the 49 KB table is shared by more threads per CTA
-#ifndef VC3_DECOMP_THREADS
-#define VC3_DECOMP_THREADS 512
-#endif
-#ifndef VC3_DECOMP_MIN_BLOCKS
-#define VC3_DECOMP_MIN_BLOCKS 2
-#endif
-
-
-// grid for `items` work items of one thread each: at most `per_sm` CTAs per
-// SM (grid-stride beyond that), at least one.
-unsigned grid_for(int64_t items, int per_sm = 8) {
-    int64_t blocks = (items + kThreads - 1) / kThreads;
-    int64_t cap = (int64_t)sm_count() * per_sm;
-    if (blocks > cap) blocks = cap;
-    return (unsigned)(blocks < 1 ? 1 : blocks);
-}
-
-// launch a table kernel: opt in to its shared-memory size first
-#define VC3_LAUNCH_TABLE(KERNEL, GRID, SMEM, STREAM, ...)                          \
-    do {                                                                           \
-        const int st_ = ensure_smem((const void*)(KERNEL), (SMEM));                \
-        if (st_) return st_;                                                       \
-        KERNEL<<<(GRID), kThreads, (SMEM), (STREAM)>>>(__VA_ARGS__);               \
-    } while (0)
-
-inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
-inline bool aligned32(const void* p) { return ((uintptr_t)p & 31u) == 0; }
-
-// ----- streaming loads/stores (read-once data: keep it out of L1) ----------
-__device__ __forceinline__ ulonglong2 ld_stream_u2(const unsigned long long* p) {
-    ulonglong2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0, %1}, [%2];"
-                 : "=l"(v.x), "=l"(v.y)
-                 : "l"(p));
-    return v;
-}
-__device__ __forceinline__ float4 ld_stream_f4(const float* p) {
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p));
-    return v;
-}
-// sm_100 256-bit global accesses (LDG/STG .256): four words per instruction
-struct u64x4 {
-    unsigned long long x, y, z, w;
-};
-__device__ __forceinline__ u64x4 ld_stream_u4(const unsigned long long* p) {
-    u64x4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0, %1, %2, %3}, [%4];"
-                 : "=l"(v.x), "=l"(v.y), "=l"(v.z), "=l"(v.w)
-                 : "l"(p));
-    return v;
-}
-__device__ __forceinline__ void st_u4(unsigned long long* p, unsigned long long a,
-                                      unsigned long long b, unsigned long long c,
-                                      unsigned long long d) {
-    asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
-                 "l"(d)
-                 : "memory");
-}
-__device__ __forceinline__ void st_u2(unsigned long long* p, unsigned long long a,
-                                      unsigned long long b) {
-    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
-}
-__device__ __forceinline__ void st_f4(float* p, float a, float b, float c, float d) {
-    asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
-                 "f"(d)
-                 : "memory");
-}
-
-__device__ __forceinline__ int64_t gtid() {
-    return (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-}
-__device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
-
-// Copy the decode table into shared memory (once per CTA; grids are capped
-// at a few CTAs per SM, so the copy is amortised over the whole stream).
-// the decode's boundary tolerance (relative to the magnitude), stored after
-// the reference's tables by get_full_table
-// CELL: the cell test (needs_exact<true>) takes the doubled tolerance
-template <bool CELL = false>
-__device__ __forceinline__ double exact_tol(const double2* __restrict__ full, const Params& P) {
-    const double t = full ? __ldg(full + (P.ntmax + 1) + (P.npmax + 1)).x : 0.0;
-    return CELL ? __dadd_rn(t, t) : t;
-}
-
-template <bool TABLE>
-__device__ __forceinline__ void load_table(double2* sm, const double2* __restrict__ g,
-                                           const Params& P) {
-    if (TABLE) {
-        const int n = P.tab_n;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = g[i];
-        __syncthreads();
-    }
-}
 
 // ===================== kernels ==============================================
 
@@ -474,7 +346,10 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_compress(con
 }
 
 // K2 decompress: 4 words (32 B in, 48 B out) per thread per step.
-template <bool TABLE, class LAY>
+// EXACT: bit-identical to the reference's libm decode (boundary components
+// redone from its own tables); !EXACT: the fast table decode, each component
+// the reference's float32 or one ulp from it.
+template <bool TABLE, class LAY, bool EXACT = true>
 __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_decompress(const unsigned long long* __restrict__ w,
                                                          float* __restrict__ xyz, int64_t n,
                                                          Params Pin, bool vec,
@@ -486,7 +361,7 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
-    const double tol = exact_tol(full, P);
+    const double tol = EXACT ? exact_tol(full, P) : 0.0;
     const int64_t groups = vec ? n / 4 : 0;
 #if VC3_DECOMP_STAGE
     // per-warp shared staging of the array-of-structs output: each lane's 48 B
@@ -506,10 +381,10 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
         const int64_t gn = g + gstride();
         if (gn < groups) wn = ld_stream_u4(w + 4 * gn);
         float o[12];
-        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.x, P, tt, tp, o[0], o[1], o[2], full, tol);
-        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.y, P, tt, tp, o[3], o[4], o[5], full, tol);
-        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.z, P, tt, tp, o[6], o[7], o[8], full, tol);
-        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(u.w, P, tt, tp, o[9], o[10], o[11], full, tol);
+        decompress_one<TABLE, false, EXACT>(u.x, P, tt, tp, o[0], o[1], o[2], full, tol);
+        decompress_one<TABLE, false, EXACT>(u.y, P, tt, tp, o[3], o[4], o[5], full, tol);
+        decompress_one<TABLE, false, EXACT>(u.z, P, tt, tp, o[6], o[7], o[8], full, tol);
+        decompress_one<TABLE, false, EXACT>(u.w, P, tt, tp, o[9], o[10], o[11], full, tol);
 #if VC3_DECOMP_STAGE
         stage[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
         stage[3 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
@@ -537,53 +412,11 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float x, y, z;
-        decompress_one<TABLE, false, VC3_DECOMP_EXACT>(w[i], P, tt, tp, x, y, z, full, tol);
+        decompress_one<TABLE, false, EXACT>(w[i], P, tt, tp, x, y, z, full, tol);
         xyz[3 * i] = x;
         xyz[3 * i + 1] = y;
         xyz[3 * i + 2] = z;
     }
-}
-
-// K3 fused add: c = compress(decompress(a) + decompress(b)) (_kernels.py:348-359)
-template <unsigned POLICY, bool TABLE>
-__device__ __forceinline__ unsigned long long add_one(unsigned long long a, unsigned long long b,
-                                                      const Params& P, const double2* tt,
-                                                      const double2* tp, const double2* full,
-                                                      double tol) {
-    float x1, y1, z1, x2, y2, z2;
-    decompress_one<TABLE, true, VC3_FUSED_EXACT>(a, P, tt, tp, x1, y1, z1, full, tol);
-    decompress_one<TABLE, true, VC3_FUSED_EXACT>(b, P, tt, tp, x2, y2, z2, full, tol);
-    return compress_one<POLICY, kFma, TABLE>(__fadd_rn(x1, x2), __fadd_rn(y1, y2), __fadd_rn(z1, z2), P);
-}
-
-template <unsigned POLICY, bool TABLE, class LAY>
-__global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_add(const unsigned long long* __restrict__ a,
-                                                  const unsigned long long* __restrict__ b,
-                                                  unsigned long long* __restrict__ c, int64_t n,
-                                                  Params Pin, bool vec,
-                                                  const double2* __restrict__ gtab,
-                                                  const double2* __restrict__ full) {
-    Params P = Pin;
-    LAY::apply(P);
-    extern __shared__ double2 s_tab[];
-    load_table<TABLE>(s_tab, gtab, P);
-    const double2* tt = s_tab;
-    const double2* tp = s_tab + P.p_base;
-    const double tol = exact_tol<VC3_CELL_CHECK>(full, P);
-    // four independent vectors per thread step give the scheduler ILP across
-    // the long FP64 chains; words move with sm_100 256-bit accesses
-    constexpr int kV = 4;  // one 32-byte load per operand and one 32-byte store per step
-    const int64_t groups = vec ? n / kV : 0;
-    for (int64_t g = gtid(); g < groups; g += gstride()) {
-        const u64x4 u = ld_stream_u4(a + kV * g), v = ld_stream_u4(b + kV * g);
-        const unsigned long long c0 = add_one<POLICY, TABLE>(u.x, v.x, P, tt, tp, full, tol);
-        const unsigned long long c1 = add_one<POLICY, TABLE>(u.y, v.y, P, tt, tp, full, tol);
-        const unsigned long long c2 = add_one<POLICY, TABLE>(u.z, v.z, P, tt, tp, full, tol);
-        const unsigned long long c3 = add_one<POLICY, TABLE>(u.w, v.w, P, tt, tp, full, tol);
-        st_u4(c + kV * g, c0, c1, c2, c3);
-    }
-    for (int64_t i = groups * kV + gtid(); i < n; i += gstride())
-        c[i] = add_one<POLICY, TABLE>(a[i], b[i], P, tt, tp, full, tol);
 }
 
 // K5 uncompressed baseline: flat float32 add (_kernels.py:341-345)
@@ -624,97 +457,6 @@ __global__ void __launch_bounds__(kThreads) k_rk_f32(float ca, float cb, float d
         const float d = __fadd_rn(__fmul_rn(ca, dq[i]), __fmul_rn(dt, R[i]));
         dq[i] = d;
         q[i] = __fadd_rn(q[i], __fmul_rn(cb, d));
-    }
-}
-
-// K4 axpy: y' = compress(alpha*decode(x) + decode(y))
-template <unsigned POLICY, bool TABLE>
-__device__ __forceinline__ unsigned long long axpy_one(float al, unsigned long long x,
-                                                       unsigned long long y, const Params& P,
-                                                       const double2* tt, const double2* tp,
-                                                       const double2* full, double tol) {
-    float x1, y1, z1, x2, y2, z2;
-    decompress_one<TABLE, true, VC3_FUSED_EXACT>(x, P, tt, tp, x1, y1, z1, full, tol);
-    decompress_one<TABLE, true, VC3_FUSED_EXACT>(y, P, tt, tp, x2, y2, z2, full, tol);
-    return compress_one<POLICY, kFma, TABLE>(__fadd_rn(__fmul_rn(al, x1), x2),
-                                      __fadd_rn(__fmul_rn(al, y1), y2),
-                                      __fadd_rn(__fmul_rn(al, z1), z2), P);
-}
-
-template <unsigned POLICY, bool TABLE, class LAY>
-__global__ void __launch_bounds__(kThreads) k_axpy(float al, const unsigned long long* __restrict__ x,
-                                                   const unsigned long long* y,
-                                                   unsigned long long* yo, int64_t n, Params Pin,
-                                                   bool vec, const double2* __restrict__ gtab,
-                                                   const double2* __restrict__ full) {
-    Params P = Pin;
-    LAY::apply(P);
-    extern __shared__ double2 s_tab[];
-    load_table<TABLE>(s_tab, gtab, P);
-    const double2* tt = s_tab;
-    const double2* tp = s_tab + P.p_base;
-    const double tol = exact_tol<VC3_CELL_CHECK>(full, P);
-    const int64_t pairs = vec ? n / 2 : 0;
-    for (int64_t g = gtid(); g < pairs; g += gstride()) {
-        const ulonglong2 u = ld_stream_u2(x + 2 * g);
-        const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(y + 2 * g);  // may alias yo
-        st_u2(yo + 2 * g, axpy_one<POLICY, TABLE>(al, u.x, v.x, P, tt, tp, full, tol),
-              axpy_one<POLICY, TABLE>(al, u.y, v.y, P, tt, tp, full, tol));
-    }
-    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride())
-        yo[i] = axpy_one<POLICY, TABLE>(al, x[i], y[i], P, tt, tp, full, tol);
-}
-
-// K4b low-storage RK stage: dq' = a*dq + dt*R ; q' = q + b*dq'
-template <unsigned POLICY, bool TABLE>
-__device__ __forceinline__ void rk_one(float ca, float cb, float dt, unsigned long long& q,
-                                       unsigned long long& dq, unsigned long long r,
-                                       const Params& P, const double2* tt, const double2* tp,
-                                       const double2* full, double tol) {
-    float q0, q1, q2, d0, d1, d2, r0, r1, r2;
-    decompress_one<TABLE, true, VC3_FUSED_EXACT, VC3_RK_CELL>(q, P, tt, tp, q0, q1, q2, full, tol);
-    decompress_one<TABLE, true, VC3_FUSED_EXACT, VC3_RK_CELL>(dq, P, tt, tp, d0, d1, d2, full, tol);
-    decompress_one<TABLE, true, VC3_FUSED_EXACT, VC3_RK_CELL>(r, P, tt, tp, r0, r1, r2, full, tol);
-    d0 = __fadd_rn(__fmul_rn(ca, d0), __fmul_rn(dt, r0));
-    d1 = __fadd_rn(__fmul_rn(ca, d1), __fmul_rn(dt, r1));
-    d2 = __fadd_rn(__fmul_rn(ca, d2), __fmul_rn(dt, r2));
-    q0 = __fadd_rn(q0, __fmul_rn(cb, d0));
-    q1 = __fadd_rn(q1, __fmul_rn(cb, d1));
-    q2 = __fadd_rn(q2, __fmul_rn(cb, d2));
-    dq = compress_one<POLICY, kFma, TABLE>(d0, d1, d2, P);
-    q = compress_one<POLICY, kFma, TABLE>(q0, q1, q2, P);
-}
-
-template <unsigned POLICY, bool TABLE, class LAY>
-__global__ void __launch_bounds__(kThreads) k_rk(float ca, float cb, float dt,
-                                                 unsigned long long* __restrict__ q,
-                                                 unsigned long long* __restrict__ dq,
-                                                 const unsigned long long* __restrict__ R,
-                                                 int64_t n, Params Pin, bool vec,
-                                                 const double2* __restrict__ gtab,
-                                                 const double2* __restrict__ full) {
-    Params P = Pin;
-    LAY::apply(P);
-    extern __shared__ double2 s_tab[];
-    load_table<TABLE>(s_tab, gtab, P);
-    const double2* tt = s_tab;
-    const double2* tp = s_tab + P.p_base;
-    const double tol = exact_tol(full, P);
-    const int64_t pairs = vec ? n / 2 : 0;
-    for (int64_t g = gtid(); g < pairs; g += gstride()) {
-        ulonglong2 u = *reinterpret_cast<const ulonglong2*>(q + 2 * g);
-        ulonglong2 v = *reinterpret_cast<const ulonglong2*>(dq + 2 * g);
-        const ulonglong2 r = ld_stream_u2(R + 2 * g);
-        rk_one<POLICY, TABLE>(ca, cb, dt, u.x, v.x, r.x, P, tt, tp, full, tol);
-        rk_one<POLICY, TABLE>(ca, cb, dt, u.y, v.y, r.y, P, tt, tp, full, tol);
-        st_u2(q + 2 * g, u.x, u.y);
-        st_u2(dq + 2 * g, v.x, v.y);
-    }
-    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride()) {
-        unsigned long long qq = q[i], dd = dq[i];
-        rk_one<POLICY, TABLE>(ca, cb, dt, qq, dd, R[i], P, tt, tp, full, tol);
-        q[i] = qq;
-        dq[i] = dd;
     }
 }
 
@@ -901,21 +643,6 @@ __global__ void k_err_final(const Moments* __restrict__ part, int64_t nchunks,
     }
 }
 
-// ----- dispatch helpers ----------------------------------------------------------
-template <template <unsigned> class F, typename... A>
-int by_policy(uint32_t pol, A... args) {
-    switch (pol & 7u) {
-        case 0: return F<0>::run(args...);
-        case 1: return F<1>::run(args...);
-        case 2: return F<2>::run(args...);
-        case 3: return F<3>::run(args...);
-        case 4: return F<4>::run(args...);
-        case 5: return F<5>::run(args...);
-        case 6: return F<6>::run(args...);
-        default: return F<7>::run(args...);
-    }
-}
-
 template <unsigned POL>
 struct RunCompress {
     static int run(const float* x, uint64_t* w, int64_t n, const Params& P, bool def, int32_t* nf,
@@ -941,72 +668,6 @@ struct RunCompress {
     }
 };
 
-// the reference's decode tables for the fused kernels' exact redo
-int fused_full_table(const Params& P, const double2** full) {
-    *full = nullptr;
-    return (VC3_FUSED_EXACT && P.table_mode) ? get_full_table(P, full) : 0;
-}
-
-template <unsigned POL>
-struct RunAdd {
-    static int run(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t n, const Params& P,
-                   bool def, const double2* tab, cudaStream_t s) {
-        auto A = (const unsigned long long*)a, B = (const unsigned long long*)b;
-        auto C = (unsigned long long*)c;
-        const bool vec = aligned32(a) && aligned32(b) && aligned32(c);
-        const unsigned grid = grid_for(vec ? (n + 3) / 4 : n, VC3_ADD_CTAS_PER_SM);
-        const double2* full = nullptr;
-        if (const int st = fused_full_table(P, &full)) return st;
-        if (def)
-            VC3_LAUNCH_TABLE((k_add<POL, true, DefaultLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab, full);
-        else if (P.table_mode)
-            VC3_LAUNCH_TABLE((k_add<POL, true, RuntimeLayout>), grid, table_smem(P), s, A, B, C, n, P, vec, tab, full);
-        else
-            k_add<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(A, B, C, n, P, vec, tab, full);
-        return launch_status();
-    }
-};
-
-template <unsigned POL>
-struct RunAxpy {
-    static int run(float al, const uint64_t* x, const uint64_t* y, uint64_t* yo, int64_t n,
-                   const Params& P, bool def, const double2* tab, cudaStream_t s) {
-        auto X = (const unsigned long long*)x, Y = (const unsigned long long*)y;
-        auto O = (unsigned long long*)yo;
-        const bool vec = aligned16(x) && aligned16(y) && aligned16(yo);
-        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n, VC3_ADD_CTAS_PER_SM);
-        const double2* full = nullptr;
-        if (const int st = fused_full_table(P, &full)) return st;
-        if (def)
-            VC3_LAUNCH_TABLE((k_axpy<POL, true, DefaultLayout>), grid, table_smem(P), s, al, X, Y, O, n, P, vec, tab, full);
-        else if (P.table_mode)
-            VC3_LAUNCH_TABLE((k_axpy<POL, true, RuntimeLayout>), grid, table_smem(P), s, al, X, Y, O, n, P, vec, tab, full);
-        else
-            k_axpy<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(al, X, Y, O, n, P, vec, tab, full);
-        return launch_status();
-    }
-};
-
-template <unsigned POL>
-struct RunRk {
-    static int run(float ca, float cb, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
-                   int64_t n, const Params& P, bool def, const double2* tab, cudaStream_t s) {
-        auto Q = (unsigned long long*)q, D = (unsigned long long*)dq;
-        auto RR = (const unsigned long long*)R;
-        const bool vec = aligned16(q) && aligned16(dq) && aligned16(R);
-        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n, VC3_ADD_CTAS_PER_SM);
-        const double2* full = nullptr;
-        if (const int st = fused_full_table(P, &full)) return st;
-        if (def)
-            VC3_LAUNCH_TABLE((k_rk<POL, true, DefaultLayout>), grid, table_smem(P), s, ca, cb, dt, Q, D, RR, n, P, vec, tab, full);
-        else if (P.table_mode)
-            VC3_LAUNCH_TABLE((k_rk<POL, true, RuntimeLayout>), grid, table_smem(P), s, ca, cb, dt, Q, D, RR, n, P, vec, tab, full);
-        else
-            k_rk<POL, false, RuntimeLayout><<<grid, kThreads, 0, s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab, full);
-        return launch_status();
-    }
-};
-
 template <unsigned POL>
 struct RunSpherical {
     static int run(const float* x, double* r, double* t, double* p, int64_t n, int32_t* nf,
@@ -1015,10 +676,6 @@ struct RunSpherical {
         return launch_status();
     }
 };
-
-#define VC3_CHECK_N(n) \
-    if ((n) < 0) return VC3_ERR_ARG; \
-    if ((n) == 0) return VC3_OK;
 
 }  // namespace
 
@@ -1080,16 +737,19 @@ int vc3_decode_tolerance(vc3_layout layout, double* tol) {
     return st;
 }
 
-int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout, void* stream) {
+int vc3_decompress_ex(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout,
+                      uint32_t flags, void* stream) {
     if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    if (flags & ~VC3_FLAGS_ALL) return VC3_ERR_ARG;
     VC3_CHECK_N(n);
     if (!xyz || !words) return VC3_ERR_ARG;
     const Params P = make_params(layout);
     const double2* tab = nullptr;
     int st = get_table(P, &tab);
     if (st) return st;
+    const bool exact = !(flags & VC3_CONTRACT);
     const double2* full = nullptr;
-    if (VC3_DECOMP_EXACT) {
+    if (exact) {
         st = get_full_table(P, &full);
         if (st) return st;
     }
@@ -1101,33 +761,25 @@ int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layo
     const unsigned grid = (unsigned)(blocks > cap ? cap : (blocks < 1 ? 1 : blocks));
     cudaStream_t s = (cudaStream_t)stream;
     const size_t stage = VC3_DECOMP_STAGE ? (size_t)VC3_DECOMP_THREADS * 48 : 0;  // 1.5 KB per warp
-    const void* fn = is_default_layout(layout) ? (const void*)k_decompress<true, DefaultLayout>
-                     : P.table_mode           ? (const void*)k_decompress<true, RuntimeLayout>
-                                              : (const void*)k_decompress<false, RuntimeLayout>;
-    const size_t smem = (P.table_mode ? table_smem(P) : 0) + stage;
-    st = ensure_smem(fn, smem);
-    if (st) return st;
-    if (is_default_layout(layout))
-        k_decompress<true, DefaultLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab, full);
-    else if (P.table_mode)
-        k_decompress<true, RuntimeLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab, full);
+    const bool def = is_default_layout(layout);
+    using KFn = void (*)(const unsigned long long*, float*, int64_t, Params, bool, const double2*,
+                         const double2*);
+    KFn fn;
+    if (!P.table_mode)  // wide layouts: the reference-angle polynomial (no table, no exactness test)
+        fn = k_decompress<false, RuntimeLayout>;
+    else if (def)
+        fn = exact ? k_decompress<true, DefaultLayout, true> : k_decompress<true, DefaultLayout, false>;
     else
-        k_decompress<false, RuntimeLayout><<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab, full);
+        fn = exact ? k_decompress<true, RuntimeLayout, true> : k_decompress<true, RuntimeLayout, false>;
+    const size_t smem = (P.table_mode ? table_smem(P) : 0) + stage;
+    st = ensure_smem((const void*)fn, smem);
+    if (st) return st;
+    fn<<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab, full);
     return launch_status();
 }
 
-int vc3_add_compressed(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t n,
-                       vc3_layout layout, uint32_t policy, void* stream) {
-    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
-    if (policy > 7u) return VC3_ERR_ARG;
-    VC3_CHECK_N(n);
-    if (!a || !b || !c) return VC3_ERR_ARG;
-    const Params P = make_params(layout);
-    const double2* tab = nullptr;
-    int st = get_table(P, &tab);
-    if (st) return st;
-    return by_policy<RunAdd>(policy, a, b, c, n, P, is_default_layout(layout), tab,
-                             (cudaStream_t)stream);
+int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout, void* stream) {
+    return vc3_decompress_ex(words, xyz, n, layout, VC3_EXACT, stream);
 }
 
 int vc3_add_raw(const float* a, const float* b, float* c, int64_t n_floats, void* stream) {
@@ -1137,34 +789,6 @@ int vc3_add_raw(const float* a, const float* b, float* c, int64_t n_floats, void
     k_add_raw<<<grid_for(vec ? (n_floats + 3) / 4 : n_floats), kThreads, 0, (cudaStream_t)stream>>>(
         a, b, c, n_floats, vec);
     return launch_status();
-}
-
-int vc3_axpy(float alpha, const uint64_t* x, const uint64_t* y, uint64_t* y_out, int64_t n,
-             vc3_layout layout, uint32_t policy, void* stream) {
-    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
-    if (policy > 7u) return VC3_ERR_ARG;
-    VC3_CHECK_N(n);
-    if (!x || !y || !y_out) return VC3_ERR_ARG;
-    const Params P = make_params(layout);
-    const double2* tab = nullptr;
-    int st = get_table(P, &tab);
-    if (st) return st;
-    return by_policy<RunAxpy>(policy, alpha, x, y, y_out, n, P, is_default_layout(layout), tab,
-                              (cudaStream_t)stream);
-}
-
-int vc3_rk_stage(float a, float b, float dt, uint64_t* q, uint64_t* dq, const uint64_t* R,
-                 int64_t n, vc3_layout layout, uint32_t policy, void* stream) {
-    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
-    if (policy > 7u) return VC3_ERR_ARG;
-    VC3_CHECK_N(n);
-    if (!q || !dq || !R) return VC3_ERR_ARG;
-    const Params P = make_params(layout);
-    const double2* tab = nullptr;
-    int st = get_table(P, &tab);
-    if (st) return st;
-    return by_policy<RunRk>(policy, a, b, dt, q, dq, R, n, P, is_default_layout(layout), tab,
-                            (cudaStream_t)stream);
 }
 
 int vc3_rk_stage_f32(float a, float b, float dt, float* q, float* dq, const float* R,
