@@ -32,6 +32,26 @@ def stream_of(t) -> int:
     return torch.cuda.current_stream(t.device).cuda_stream
 
 
+class on_device:
+    """Make ``t``'s CUDA device current around a C-ABI call: the library
+    launches on the current device and keys its decode tables by it, so a
+    tensor on another GPU than the current one needs the switch
+    (torch.cuda.device guard; a no-op for host operands)."""
+
+    def __init__(self, t):
+        self._ctx = torch.cuda.device(t.device) if is_device(t) else None
+
+    def __enter__(self):
+        if self._ctx is not None:
+            self._ctx.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        if self._ctx is not None:
+            self._ctx.__exit__(*exc)
+        return False
+
+
 def ptr(x) -> int:
     if isinstance(x, np.ndarray):
         return x.ctypes.data

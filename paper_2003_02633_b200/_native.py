@@ -84,6 +84,16 @@ SIGNATURES = {
 # numerics modes of the *_ex entry points (include/vc3_b200.h)
 VC3_EXACT = 0
 VC3_CONTRACT = 1
+MODES = {"exact": VC3_EXACT, "contract": VC3_CONTRACT}
+
+
+def mode_flag(mode: str) -> int:
+    """``"exact"`` (bit-identical to the reference, the default) or
+    ``"contract"`` (the north-star tolerance: one-ulp decodes, one-bin ties)."""
+    try:
+        return MODES[mode]
+    except KeyError:
+        raise ValueError(f"mode must be one of {sorted(MODES)}, got {mode!r}") from None
 
 VC3_OK = 0
 VC3_ERR_LAYOUT = -1

@@ -139,21 +139,29 @@ def compress_with_events(vectors, layout=DEFAULT_LAYOUT, policy=DEFAULT_POLICY):
     return (_dev.download(out) if host else out), (int(counts[0]), int(counts[1]))
 
 
-def decompress(words, layout=DEFAULT_LAYOUT):
+def decompress(words, layout=DEFAULT_LAYOUT, mode="exact"):
     """Reconstruct (n, 3) float32 vectors from packed words (codec.py:205-228).
 
     Every word decodes to a finite vector; a zero magnitude field decodes to
-    (0, 0, 0) whatever the angle bits."""
+    (0, 0, 0) whatever the angle bits.  ``mode="exact"`` (default) is
+    bit-identical to the reference's decode; ``mode="contract"`` skips the
+    boundary re-evaluation (each component the reference's float32 or one ulp
+    from it)."""
     layout = as_layout(layout)
+    flags = _native.mode_flag(mode)
     lib = _native.load()
     if _dev.is_device(words):
         w = _device_words(words)
         n = w.shape[0]
         out = torch.empty((n, 3), dtype=torch.float32, device=w.device)
-        _native.check(lib.vc3_decompress(w.data_ptr(), out.data_ptr(), n,
-                                         _native.c_layout(layout), _dev.stream_of(w)),
-                      "decompress")
+        with _dev.on_device(w):
+            _native.check(lib.vc3_decompress_ex(w.data_ptr(), out.data_ptr(), n,
+                                                _native.c_layout(layout), flags,
+                                                _dev.stream_of(w)), "decompress")
         return out
+    if flags:
+        return _dev.download(decompress(_dev.upload(np.asarray(words, dtype=np.uint64).ravel()),
+                                        layout, mode))
     w = np.ascontiguousarray(np.asarray(words, dtype=np.uint64).ravel())
     out = np.empty((w.size, 3), dtype=np.float32)
     _native.check(lib.vc3_decompress_host(w.ctypes.data, out.ctypes.data, w.size,

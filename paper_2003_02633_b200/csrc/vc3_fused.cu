@@ -21,9 +21,23 @@
 
 #include "../../include/vc3_b200.h"
 #include "vc3_device.cuh"
-#include "vc3_fused.cuh"
 #include "vc3_kern_common.cuh"
 #include "vc3_rt.h"
+
+// the all-single kernels live in vc3_fused_as.cu
+namespace vc3 {
+namespace as {
+int launch_add(const unsigned long long* a, const unsigned long long* b, unsigned long long* c,
+               int64_t n, const Params& P, bool def, bool exact, bool vec, const double2* tab,
+               const double2* full, cudaStream_t s);
+int launch_axpy(float al, const unsigned long long* x, const unsigned long long* y,
+                unsigned long long* yo, int64_t n, const Params& P, bool def, bool exact, bool vec,
+                const double2* tab, const double2* full, cudaStream_t s);
+int launch_rk(float ca, float cb, float dt, unsigned long long* q, unsigned long long* dq,
+              const unsigned long long* R, int64_t n, const Params& P, bool def, bool exact,
+              bool vec, const double2* tab, const double2* full, cudaStream_t s);
+}  // namespace as
+}  // namespace vc3
 
 #ifndef VC3_USE_FMA
 #define VC3_USE_FMA 1
@@ -170,83 +184,6 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS)
     }
 }
 
-// ===================== all-single path on table layouts ======================
-// Four vectors per thread step: eight fast table decodes, float32 sums, two
-// compress_as2 pairs.  The rare exceptions take warp-uniform branches (one
-// vote each per step, so the exception code is never predicated into the
-// hot path): the exact mode's boundary redo (decode_redo, ~1e-5 of words) and
-// the compress range exceptions (the generic bit-exact compress_one).
-template <bool EXACT>
-__device__ __forceinline__ void decode4(const unsigned long long w[4], const Params& P,
-                                        const double2* tt, const double2* tp, const double2* full,
-                                        double tol2, float x[4], float y[4], float z[4]) {
-    unsigned redo = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-        redo |= (unsigned)decode_fused<EXACT>(w[k], P, tt, tp, tol2, x[k], y[k], z[k]) << k;
-    if (EXACT && __any_sync(__activemask(), redo != 0u)) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if ((redo >> k) & 1u) decode_redo(w[k], P, full, x[k], y[k], z[k]);
-    }
-}
-
-__device__ __forceinline__ void encode4(const float x[4], const float y[4], const float z[4],
-                                        const Params& P, unsigned long long w[4]) {
-    bool slow[4];
-    compress_as2(x, y, z, P, w, slow);
-    compress_as2(x + 2, y + 2, z + 2, P, w + 2, slow + 2);
-    if (__any_sync(__activemask(), slow[0] | slow[1] | slow[2] | slow[3])) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (slow[k]) w[k] = compress_one<kAllSingle, true, true>(x[k], y[k], z[k], P);
-    }
-}
-
-// float32 sums of two decoded pairs (one FADD2 per component pair)
-__device__ __forceinline__ void add_pairs(const float a[2], const float b[2], float out[2]) {
-    upk(add2(pk(a[0], a[1]), pk(b[0], b[1])), out[0], out[1]);
-}
-
-template <bool EXACT, class LAY>
-__global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS)
-    k_add_as(const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
-             unsigned long long* __restrict__ c, int64_t n, Params Pin, bool vec,
-             const double2* __restrict__ gtab, const double2* __restrict__ full) {
-    Params P = Pin;
-    LAY::apply(P);
-    extern __shared__ double2 s_tab[];
-    load_table<true>(s_tab, gtab, P);
-    const double2* tt = s_tab;
-    const double2* tp = s_tab + P.p_base;
-    const double tol2 = EXACT ? exact_tol<true>(full, P) : 0.0;
-    const int64_t groups = vec ? n / 4 : 0;
-    for (int64_t g = gtid(); g < groups; g += gstride()) {
-        const u64x4 u = ld_stream_u4(a + 4 * g), v = ld_stream_u4(b + 4 * g);
-        const unsigned long long wa[4] = {u.x, u.y, u.z, u.w}, wb[4] = {v.x, v.y, v.z, v.w};
-        float xa[4], ya[4], za[4], xb[4], yb[4], zb[4], x[4], y[4], z[4];
-        decode4<EXACT>(wa, P, tt, tp, full, tol2, xa, ya, za);
-        decode4<EXACT>(wb, P, tt, tp, full, tol2, xb, yb, zb);
-#pragma unroll
-        for (int k = 0; k < 4; k += 2) {
-            add_pairs(xa + k, xb + k, x + k);
-            add_pairs(ya + k, yb + k, y + k);
-            add_pairs(za + k, zb + k, z + k);
-        }
-        unsigned long long w[4];
-        encode4(x, y, z, P, w);
-        st_u4(c + 4 * g, w[0], w[1], w[2], w[3]);
-    }
-    for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
-        float x1, y1, z1, x2, y2, z2;
-        const unsigned long long wa = a[i], wb = b[i];
-        if (decode_fused<EXACT>(wa, P, tt, tp, tol2, x1, y1, z1)) decode_redo(wa, P, full, x1, y1, z1);
-        if (decode_fused<EXACT>(wb, P, tt, tp, tol2, x2, y2, z2)) decode_redo(wb, P, full, x2, y2, z2);
-        c[i] = compress_one<kAllSingle, true, true>(__fadd_rn(x1, x2), __fadd_rn(y1, y2),
-                                                    __fadd_rn(z1, z2), P);
-    }
-}
-
 // ===================== dispatch ================================================
 int full_table_for(const Params& P, bool exact, const double2** full) {
     *full = nullptr;
@@ -260,12 +197,12 @@ struct AddKernel {
                         int64_t, Params, bool, const double2*, const double2*);
     static Fn pick(const Params& P, bool def, bool exact) {
         if (!P.table_mode) return k_add<POL, false, RuntimeLayout, true>;
-        if (POL == kAllSingle) {
-            if (def) return exact ? k_add_as<true, DefaultLayout> : k_add_as<false, DefaultLayout>;
-            return exact ? k_add_as<true, RuntimeLayout> : k_add_as<false, RuntimeLayout>;
+        if constexpr (POL == kAllSingle) {
+            return nullptr;  // table layouts: vc3::as::launch_add (vc3_fused_as.cu)
+        } else {
+            if (def) return exact ? k_add<POL, true, DefaultLayout, true> : k_add<POL, true, DefaultLayout, false>;
+            return exact ? k_add<POL, true, RuntimeLayout, true> : k_add<POL, true, RuntimeLayout, false>;
         }
-        if (def) return exact ? k_add<POL, true, DefaultLayout, true> : k_add<POL, true, DefaultLayout, false>;
-        return exact ? k_add<POL, true, RuntimeLayout, true> : k_add<POL, true, RuntimeLayout, false>;
     }
 };
 
@@ -277,6 +214,9 @@ struct RunAdd {
         const unsigned grid = grid_for(vec ? (n + 3) / 4 : n, VC3_ADD_CTAS_PER_SM);
         const double2* full = nullptr;
         if (const int st = full_table_for(P, exact, &full)) return st;
+        if (POL == kAllSingle && P.table_mode)
+            return vc3::as::launch_add((const unsigned long long*)a, (const unsigned long long*)b,
+                                       (unsigned long long*)c, n, P, def, exact, vec, tab, full, s);
         const auto fn = AddKernel<POL>::pick(P, def, exact);
         const size_t smem = table_smem(P);
         if (const int st = ensure_smem((const void*)fn, smem)) return st;
@@ -292,16 +232,23 @@ struct RunAxpy {
                    const Params& P, bool def, bool exact, const double2* tab, cudaStream_t s) {
         auto X = (const unsigned long long*)x, Y = (const unsigned long long*)y;
         auto O = (unsigned long long*)yo;
-        const bool vec = aligned16(x) && aligned16(y) && aligned16(yo);
-        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n, VC3_ADD_CTAS_PER_SM);
         const double2* full = nullptr;
         if (const int st = full_table_for(P, exact, &full)) return st;
+        if (POL == kAllSingle && P.table_mode)
+            return vc3::as::launch_axpy(al, X, Y, O, n, P, def, exact,
+                                        aligned32(x) && aligned32(y) && aligned32(yo), tab, full, s);
+        const bool vec = aligned16(x) && aligned16(y) && aligned16(yo);
+        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n, VC3_ADD_CTAS_PER_SM);
         using Fn = void (*)(float, const unsigned long long*, const unsigned long long*,
                             unsigned long long*, int64_t, Params, bool, const double2*, const double2*);
         Fn fn;
-        if (!P.table_mode) fn = k_axpy<POL, false, RuntimeLayout, true>;
-        else if (def) fn = exact ? k_axpy<POL, true, DefaultLayout, true> : k_axpy<POL, true, DefaultLayout, false>;
-        else fn = exact ? k_axpy<POL, true, RuntimeLayout, true> : k_axpy<POL, true, RuntimeLayout, false>;
+        if constexpr (POL == kAllSingle) {
+            fn = k_axpy<POL, false, RuntimeLayout, true>;  // wide layouts only (tables: vc3_fused_as.cu)
+        } else {
+            if (!P.table_mode) fn = k_axpy<POL, false, RuntimeLayout, true>;
+            else if (def) fn = exact ? k_axpy<POL, true, DefaultLayout, true> : k_axpy<POL, true, DefaultLayout, false>;
+            else fn = exact ? k_axpy<POL, true, RuntimeLayout, true> : k_axpy<POL, true, RuntimeLayout, false>;
+        }
         const size_t smem = table_smem(P);
         if (const int st = ensure_smem((const void*)fn, smem)) return st;
         fn<<<grid, kThreads, smem, s>>>(al, X, Y, O, n, P, vec, tab, full);
@@ -316,17 +263,24 @@ struct RunRk {
                    cudaStream_t s) {
         auto Q = (unsigned long long*)q, D = (unsigned long long*)dq;
         auto RR = (const unsigned long long*)R;
-        const bool vec = aligned16(q) && aligned16(dq) && aligned16(R);
-        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n, VC3_ADD_CTAS_PER_SM);
         const double2* full = nullptr;
         if (const int st = full_table_for(P, exact, &full)) return st;
+        if (POL == kAllSingle && P.table_mode)
+            return vc3::as::launch_rk(ca, cb, dt, Q, D, RR, n, P, def, exact,
+                                      aligned32(q) && aligned32(dq) && aligned32(R), tab, full, s);
+        const bool vec = aligned16(q) && aligned16(dq) && aligned16(R);
+        const unsigned grid = grid_for(vec ? (n + 1) / 2 : n, VC3_ADD_CTAS_PER_SM);
         using Fn = void (*)(float, float, float, unsigned long long*, unsigned long long*,
                             const unsigned long long*, int64_t, Params, bool, const double2*,
                             const double2*);
         Fn fn;
-        if (!P.table_mode) fn = k_rk<POL, false, RuntimeLayout, true>;
-        else if (def) fn = exact ? k_rk<POL, true, DefaultLayout, true> : k_rk<POL, true, DefaultLayout, false>;
-        else fn = exact ? k_rk<POL, true, RuntimeLayout, true> : k_rk<POL, true, RuntimeLayout, false>;
+        if constexpr (POL == kAllSingle) {
+            fn = k_rk<POL, false, RuntimeLayout, true>;  // wide layouts only (tables: vc3_fused_as.cu)
+        } else {
+            if (!P.table_mode) fn = k_rk<POL, false, RuntimeLayout, true>;
+            else if (def) fn = exact ? k_rk<POL, true, DefaultLayout, true> : k_rk<POL, true, DefaultLayout, false>;
+            else fn = exact ? k_rk<POL, true, RuntimeLayout, true> : k_rk<POL, true, RuntimeLayout, false>;
+        }
         const size_t smem = table_smem(P);
         if (const int st = ensure_smem((const void*)fn, smem)) return st;
         fn<<<grid, kThreads, smem, s>>>(ca, cb, dt, Q, D, RR, n, P, vec, tab, full);

@@ -643,11 +643,23 @@ __global__ void k_err_final(const Moments* __restrict__ part, int64_t nchunks,
     }
 }
 
+}  // namespace
+namespace vc3 {
+namespace as {  // vc3_fused_as.cu
+int launch_compress(const float* xyz, unsigned long long* w, int64_t n, const Params& P, bool def,
+                    bool vec, int32_t* nonfinite, cudaStream_t s);
+}  // namespace as
+}  // namespace vc3
+namespace {
+
 template <unsigned POL>
 struct RunCompress {
     static int run(const float* x, uint64_t* w, int64_t n, const Params& P, bool def, int32_t* nf,
                    unsigned long long* ev, cudaStream_t s) {
         const bool vec = aligned16(x) && aligned32(w);
+        // all-single policy: the restructured compress of vc3_fused.cuh
+        if (POL == 7u && !ev && P.t <= 25 && P.p <= 24)
+            return vc3::as::launch_compress(x, (unsigned long long*)w, n, P, def, vec, nf, s);
         const unsigned grid = grid_for(vec ? (n + 3) / 4 : n, VC3_COMPRESS_CTAS_PER_SM);
         auto W = (unsigned long long*)w;
         if (ev) {

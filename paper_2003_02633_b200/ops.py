@@ -51,25 +51,32 @@ def add_raw(a, b):
     return _dev.download(add_raw(_dev.upload(ha), _dev.upload(hb)))
 
 
-def add_compressed(a, b, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY):
+def add_compressed(a, b, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY, mode="exact"):
     """compress(decompress(a) + decompress(b)) in one fused kernel
     (bench.py:41-69, _kernels.py:348-359).  Default policy all-single, as
-    the reference's benchmark path."""
+    the reference's benchmark path.  ``mode="contract"`` selects the
+    north-star tolerance (VC3_CONTRACT: a decoded component may be one ulp
+    off, a word may move one bin at a tie)."""
     layout, policy = as_layout(layout), as_policy(policy)
+    flags = _native.mode_flag(mode)
     lib = _native.load()
     if _dev.is_device(a):
         ta, tb = _words_dev(a), _words_dev(b.to(a.device))
         if ta.shape != tb.shape:
             raise LengthMismatch(f"lengths differ: {ta.numel()} vs {tb.numel()}")
         c = torch.empty_like(ta)
-        _native.check(lib.vc3_add_compressed(ta.data_ptr(), tb.data_ptr(), c.data_ptr(),
-                                             ta.numel(), _native.c_layout(layout), policy.mask,
-                                             _dev.stream_of(ta)), "add_compressed")
+        with _dev.on_device(ta):
+            _native.check(lib.vc3_add_compressed_ex(ta.data_ptr(), tb.data_ptr(), c.data_ptr(),
+                                                    ta.numel(), _native.c_layout(layout),
+                                                    policy.mask, flags, _dev.stream_of(ta)),
+                          "add_compressed")
         return c.reshape(a.shape)
     ha = np.ascontiguousarray(a, dtype=np.uint64)
     hb = np.ascontiguousarray(b, dtype=np.uint64)
     if ha.shape != hb.shape:
         raise LengthMismatch(f"lengths differ: {ha.size} vs {hb.size}")
+    if flags:
+        return _dev.download(add_compressed(_dev.upload(ha), _dev.upload(hb), layout, policy, mode))
     c = np.empty_like(ha)
     _native.check(lib.vc3_add_compressed_host(ha.ctypes.data, hb.ctypes.data, c.ctypes.data,
                                               ha.size, _native.c_layout(layout), policy.mask,
@@ -77,9 +84,10 @@ def add_compressed(a, b, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY):
     return c
 
 
-def axpy(alpha, x, y, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY, out=None):
+def axpy(alpha, x, y, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY, out=None, mode="exact"):
     """compress(alpha*decompress(x) + decompress(y)); ``out=y`` updates in place."""
     layout, policy = as_layout(layout), as_policy(policy)
+    flags = _native.mode_flag(mode)
     lib = _native.load()
     host = not _dev.is_device(x)
     tx = _dev.upload(np.asarray(x, dtype=np.uint64)) if host else _words_dev(x)
@@ -87,9 +95,10 @@ def axpy(alpha, x, y, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY, out=None)
     if tx.shape != ty.shape:
         raise LengthMismatch(f"lengths differ: {tx.numel()} vs {ty.numel()}")
     to = (torch.empty_like(ty) if (out is None or host) else _words_dev(out))
-    _native.check(lib.vc3_axpy(float(np.float32(alpha)), tx.data_ptr(), ty.data_ptr(),
-                               to.data_ptr(), tx.numel(), _native.c_layout(layout), policy.mask,
-                               _dev.stream_of(tx)), "axpy")
+    with _dev.on_device(tx):
+        _native.check(lib.vc3_axpy_ex(float(np.float32(alpha)), tx.data_ptr(), ty.data_ptr(),
+                                      to.data_ptr(), tx.numel(), _native.c_layout(layout),
+                                      policy.mask, flags, _dev.stream_of(tx)), "axpy")
     if host:
         res = _dev.download(to)
         if out is not None:
@@ -99,10 +108,11 @@ def axpy(alpha, x, y, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY, out=None)
     return to
 
 
-def rk_stage(a, b, dt, q, dq, R, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY):
+def rk_stage(a, b, dt, q, dq, R, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY, mode="exact"):
     """One low-storage RK stage on compressed q, dq and residual R, in place:
     dq <- a*dq + dt*R ; q <- q + b*dq.  Returns (q, dq)."""
     layout, policy = as_layout(layout), as_policy(policy)
+    flags = _native.mode_flag(mode)
     lib = _native.load()
     host = not _dev.is_device(q)
     tq = _dev.upload(np.asarray(q, dtype=np.uint64)) if host else q
@@ -112,10 +122,11 @@ def rk_stage(a, b, dt, q, dq, R, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY
         raise LengthMismatch("q, dq and R must have the same length")
     if not host and not (tq.is_contiguous() and tdq.is_contiguous()):
         raise ValueError("rk_stage updates q and dq in place: pass contiguous tensors")
-    _native.check(lib.vc3_rk_stage(float(np.float32(a)), float(np.float32(b)),
-                                   float(np.float32(dt)), tq.data_ptr(), tdq.data_ptr(),
-                                   tR.data_ptr(), tq.numel(), _native.c_layout(layout),
-                                   policy.mask, _dev.stream_of(tq)), "rk_stage")
+    with _dev.on_device(tq):
+        _native.check(lib.vc3_rk_stage_ex(float(np.float32(a)), float(np.float32(b)),
+                                          float(np.float32(dt)), tq.data_ptr(), tdq.data_ptr(),
+                                          tR.data_ptr(), tq.numel(), _native.c_layout(layout),
+                                          policy.mask, flags, _dev.stream_of(tq)), "rk_stage")
     if host:
         q[...] = _dev.download(tq)
         dq[...] = _dev.download(tdq)
@@ -150,7 +161,8 @@ class LSRKStep:
     steps.  ``step()`` is bit-identical to calling ``rk_stage`` five times.
     """
 
-    def __init__(self, q, dq, R, dt: float, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY):
+    def __init__(self, q, dq, R, dt: float, layout=DEFAULT_LAYOUT, policy=ALL_SINGLE_POLICY,
+                 mode="exact"):
         from .fields import LSRK_A, LSRK_B
 
         _dev.require_torch_cuda()
@@ -164,13 +176,15 @@ class LSRKStep:
         self._cl = _native.c_layout(self.layout)
         self._coef = [(float(np.float32(a)), float(np.float32(b))) for a, b in zip(LSRK_A, LSRK_B)]
         self._dt = float(np.float32(dt))
+        self._flags = _native.mode_flag(mode)
         self.graph = None
 
     def _launch_all(self, stream_ptr):
         for a, b in self._coef:
-            _native.check(self._lib.vc3_rk_stage(a, b, self._dt, self.q.data_ptr(), self.dq.data_ptr(),
-                                                 self.R.data_ptr(), self.q.numel(), self._cl,
-                                                 self.policy.mask, stream_ptr), "rk_stage")
+            _native.check(self._lib.vc3_rk_stage_ex(a, b, self._dt, self.q.data_ptr(),
+                                                    self.dq.data_ptr(), self.R.data_ptr(),
+                                                    self.q.numel(), self._cl, self.policy.mask,
+                                                    self._flags, stream_ptr), "rk_stage")
 
     def capture(self):
         """Record the five stages (no work is done by the capture itself)."""
@@ -181,9 +195,9 @@ class LSRKStep:
             # warm up on one-word scratch copies: the layout's decode table and
             # the kernel's shared-memory attribute are set up outside the capture
             sq, sdq, sR = self.q[:1].clone(), self.dq[:1].clone(), self.R[:1].clone()
-            _native.check(self._lib.vc3_rk_stage(1.0, 1.0, 0.0, sq.data_ptr(), sdq.data_ptr(),
-                                                 sR.data_ptr(), 1, self._cl, self.policy.mask,
-                                                 s.cuda_stream), "rk_stage")
+            _native.check(self._lib.vc3_rk_stage_ex(1.0, 1.0, 0.0, sq.data_ptr(), sdq.data_ptr(),
+                                                    sR.data_ptr(), 1, self._cl, self.policy.mask,
+                                                    self._flags, s.cuda_stream), "rk_stage")
             s.synchronize()
             with torch.cuda.graph(g, stream=s):
                 self._launch_all(s.cuda_stream)

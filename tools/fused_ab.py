@@ -113,6 +113,49 @@ def main():
         res["add"]["exact_vs_ref"] = word_deltas(c_ex, c_r)
         del c_r
     res["add"]["contract_vs_exact"] = word_deltas(c_ct, c_ex)
+    # standalone compress (the all-single fast path vs the reference build)
+    vx = torch.rand((n, 3), device=dev, generator=gen).mul_(2).sub_(1)
+    cw = torch.empty_like(a)
+    f_c = lambda: lib.vc3_compress(vx.data_ptr(), cw.data_ptr(), n, cl, pol.mask, None, sp)
+    res["compress"] = {"gvec_s": n / timeit(f_c, args.steps, stream) / 1e6}
+    if ref is not None:
+        cw2 = torch.empty_like(a)
+        f_c2 = lambda: ref.vc3_compress(vx.data_ptr(), cw2.data_ptr(), n, cl, pol.mask, None, sp)
+        res["compress"]["ref_gvec_s"] = n / timeit(f_c2, args.steps, stream) / 1e6
+        res["compress"]["equal_ref"] = bool(torch.equal(cw, cw2))
+        del cw2
+    del vx, cw
+    # axpy y' = 0.75 x + y (out of place) and the RK stage (in place, on copies)
+    for mode in (0, 1):
+        o = torch.empty_like(a)
+        f = lambda: lib.vc3_axpy_ex(0.75, a.data_ptr(), b.data_ptr(), o.data_ptr(), n, cl, pol.mask, mode, sp)
+        res.setdefault("axpy", {})[("exact" if mode == 0 else "contract") + "_gvec_s"] = n / timeit(f, args.steps, stream) / 1e6
+        if mode == 0:
+            o_ex = o
+    if ref is not None:
+        o2 = torch.empty_like(a)
+        ref.vc3_axpy(0.75, a.data_ptr(), b.data_ptr(), o2.data_ptr(), n, cl, pol.mask, sp)
+        torch.cuda.synchronize()
+        res["axpy"]["exact_equal_ref"] = bool(torch.equal(o_ex, o2))
+        del o2
+    del o, o_ex
+    q0, d0 = a.clone(), b.clone()
+    for mode in (0, 1):
+        q, d = q0.clone(), d0.clone()
+        f = lambda: lib.vc3_rk_stage_ex(0.5, 0.25, 1e-3, q.data_ptr(), d.data_ptr(), c_ex.data_ptr(), n, cl,
+                                        pol.mask, mode, sp)
+        res.setdefault("rk", {})[("exact" if mode == 0 else "contract") + "_gvec_s"] = n / timeit(f, args.steps, stream) / 1e6
+        if mode == 0:
+            q, d = q0.clone(), d0.clone()
+            f()
+            torch.cuda.synchronize()
+            q_ex, d_ex = q, d
+    if ref is not None:
+        q, d = q0.clone(), d0.clone()
+        ref.vc3_rk_stage(0.5, 0.25, 1e-3, q.data_ptr(), d.data_ptr(), c_ex.data_ptr(), n, cl, pol.mask, sp)
+        torch.cuda.synchronize()
+        res["rk"]["exact_equal_ref"] = bool(torch.equal(q, q_ex) and torch.equal(d, d_ex))
+    del q, d, q0, d0
     # decompress both modes
     out = torch.empty((n, 3), dtype=torch.float32, device=dev)
     out2 = torch.empty_like(out)
