@@ -12,7 +12,12 @@
  *   - every call is asynchronous on the caller's CUDA stream (`stream` is a
  *     cudaStream_t passed as void*; NULL = legacy default stream);
  *   - all pointers are DEVICE pointers unless the name ends in _host;
- *   - the library allocates nothing per call; callers own every buffer.
+ *   - callers own every input and output buffer.  Per call the library
+ *     allocates nothing except: vc3_error_stats (stream-ordered scratch from
+ *     the device pool; vc3_error_stats_ws takes a caller workspace instead)
+ *     and the host-buffer entry points (chunk staging from a library pool
+ *     that keeps its memory between calls).  Once per (device, layout) the
+ *     decode tables are built (vc3_prepare_layout).
  *
  * Return value: VC3_OK (0) or a negative vc3_status.  Validation happens before
  * any launch (the reference validates before its kernels, codec.py:70-83,
@@ -85,17 +90,26 @@ int vc3_compress(const float* xyz, uint64_t* words, int64_t n, vc3_layout layout
                  uint32_t policy, int32_t* d_nonfinite, void* stream);
 
 /* The bound, relative to the magnitude, by which the fast table decode's
- * components can differ from the reference's doubles (measured over every
- * table index against the reference's tables); components within it of a
- * float32 rounding boundary are re-evaluated exactly.  0 for layouts decoded
- * without tables.  Synchronous; builds the tables on first use. */
+ * components can differ from the reference's doubles (measured on the host
+ * over every table index against the reference's tables when the tables are
+ * built); components within it of a float32 rounding boundary are
+ * re-evaluated exactly.  0 for layouts decoded without tables.  Builds the
+ * tables on first use. */
 int vc3_decode_tolerance(vc3_layout layout, double* tol);
+
+/* Build the decode tables of a layout on the current device ahead of the
+ * first operation (the 49 KB fast table, and for VC3_EXACT the reference's
+ * 6 MB tables).  Optional: every operation builds them on first use, also
+ * inside a caller's CUDA-graph capture (the build uses a private stream and
+ * relaxed capture mode), but preparing keeps that one-off host work (~10 ms)
+ * out of the first call. */
+int vc3_prepare_layout(vc3_layout layout, uint32_t flags);
 
 /* codec.decompress (codec.py:205-228) -> decompress_kernel_tab/_direct
  * (_kernels.py:293-331).  words: uint64 [n]; xyz: float32 [n][3].
  * Bit-identical to the reference's decode (its libm sin/cos tables): the
  * first call for a layout builds a 49 KB shared-memory table and the 6 MB
- * reference table on the device (call once before graph capture). */
+ * reference table on the device (capture-safe; see vc3_prepare_layout). */
 int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout,
                    void* stream);
 /* vc3_decompress with a numerics mode (VC3_EXACT / VC3_CONTRACT). */
@@ -167,6 +181,11 @@ int vc3_decode_magnitude(const int64_t* field, float* r, int64_t n, vc3_layout l
  * d_counts[1] += saturated (caller zeroes them). */
 int vc3_magnitude_events(const float* xyz, int64_t n, vc3_layout layout,
                          unsigned long long* d_counts, void* stream);
+/* The same, also counting vectors with a NaN or infinite component into
+ * *d_nonfinite (device int32, zeroed by the caller; the reference raises
+ * NonFiniteInput for them, codec.py:76-78). */
+int vc3_magnitude_events_checked(const float* xyz, int64_t n, vc3_layout layout,
+                                 unsigned long long* d_counts, int32_t* d_nonfinite, void* stream);
 
 /* ---- K7 variants (analysis.py:259-417) ------------------------------------
  * Angle coding variants the reference evaluates in compand_study and
@@ -217,6 +236,11 @@ int vc3_variant_maxima(vc3_layout layout, vc3_variant variant, int64_t* n_theta_
 #define VC3_ERR_REL_MAGNITUDE 3
 int vc3_error_stats(const float* v, const float* vh, int64_t n, int32_t kind,
                     int64_t chunk, double* d_chunk_stats, void* stream);
+/* The same with a caller-provided device workspace of at least
+ * vc3_error_stats_workspace(n, chunk) bytes (no allocation at all). */
+int vc3_error_stats_workspace(int64_t n, int64_t chunk, uint64_t* bytes);
+int vc3_error_stats_ws(const float* v, const float* vh, int64_t n, int32_t kind, int64_t chunk,
+                       double* d_chunk_stats, void* d_work, uint64_t work_bytes, void* stream);
 
 /* ---- flux-reconstruction flux divergence (Alg. 1) ------
  * No reference code exists; the operation is the paper's

@@ -51,6 +51,7 @@ SIGNATURES = {
     "vc3_decompress": ([_p, _p, _i64, Layout, _p], ctypes.c_int),
     "vc3_decompress_ex": ([_p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
     "vc3_decode_tolerance": ([Layout, _p], ctypes.c_int),
+    "vc3_prepare_layout": ([Layout, _u32], ctypes.c_int),
     "vc3_compress_events": ([_p, _p, _i64, Layout, _u32, _p, _p, _p], ctypes.c_int),
     "vc3_add_compressed": ([_p, _p, _p, _i64, Layout, _u32, _p], ctypes.c_int),
     "vc3_add_compressed_ex": ([_p, _p, _p, _i64, Layout, _u32, _u32, _p], ctypes.c_int),
@@ -66,7 +67,10 @@ SIGNATURES = {
     "vc3_encode_magnitude": ([_p, _p, _i64, Layout, _p], ctypes.c_int),
     "vc3_decode_magnitude": ([_p, _p, _i64, Layout, _p], ctypes.c_int),
     "vc3_magnitude_events": ([_p, _i64, Layout, _p, _p], ctypes.c_int),
+    "vc3_magnitude_events_checked": ([_p, _i64, Layout, _p, _p, _p], ctypes.c_int),
     "vc3_error_stats": ([_p, _p, _i64, _i32, _i64, _p, _p], ctypes.c_int),
+    "vc3_error_stats_workspace": ([_i64, _i64, _p], ctypes.c_int),
+    "vc3_error_stats_ws": ([_p, _p, _i64, _i32, _i64, _p, _p, ctypes.c_uint64, _p], ctypes.c_int),
     "vc3_compress_variant": ([_p, _p, _i64, Layout, Variant, _p, _p], ctypes.c_int),
     "vc3_decompress_variant": ([_p, _p, _i64, Layout, Variant, _p], ctypes.c_int),
     "vc3_variant_maxima": ([Layout, Variant, _p, _p], ctypes.c_int),
@@ -110,8 +114,16 @@ def load() -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    # VC3_B200_AUTOBUILD: unset -> build only when the library is missing;
+    # "stale" -> also rebuild when a source is newer than it (development);
+    # "0" -> never build
+    autobuild = os.environ.get("VC3_B200_AUTOBUILD", "missing")
+    if autobuild == "stale" and "VC3_B200_LIB" not in os.environ:
+        from ._build import build
+
+        build()
     if not LIB_PATH.exists():
-        if os.environ.get("VC3_B200_AUTOBUILD", "1") == "1":
+        if autobuild != "0":
             from ._build import build
 
             build()

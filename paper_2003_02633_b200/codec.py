@@ -325,9 +325,15 @@ def magnitude_event_counts(vectors, layout=DEFAULT_LAYOUT):
     else:
         v = _device_vectors(vectors)
     counts = torch.zeros(2, dtype=torch.int64, device=v.device)
-    _native.check(lib.vc3_magnitude_events(v.data_ptr(), v.shape[0], _native.c_layout(layout),
-                                           counts.data_ptr(), _dev.stream_of(v)),
-                  "magnitude_event_counts")
+    nonfinite = torch.zeros(1, dtype=torch.int32, device=v.device)
+    with _dev.on_device(v):
+        _native.check(lib.vc3_magnitude_events_checked(v.data_ptr(), v.shape[0],
+                                                       _native.c_layout(layout), counts.data_ptr(),
+                                                       nonfinite.data_ptr(), _dev.stream_of(v)),
+                      "magnitude_event_counts")
+    bad = int(nonfinite.item())
+    if bad:
+        raise NonFiniteInput(_nonfinite_message(bad))
     c = counts.cpu().tolist()
     return int(c[0]), int(c[1])
 

@@ -29,6 +29,8 @@ constexpr int64_t kChunk = int64_t(1) << VC3_HOST_CHUNK_LOG2;  // vectors per ch
 struct DeviceCtx {
     cudaMemPool_t pool = nullptr;
     cudaStream_t streams[kStreams] = {};
+    int32_t* d_bad = nullptr;  // non-finite counter of vc3_compress_host (allocated once)
+    std::recursive_mutex call_mu;  // one host-buffer call at a time per device (shared streams)
     bool ready = false;
 };
 
@@ -51,6 +53,14 @@ int ctx_for(int device, DeviceCtx** out) {
         for (auto& s : c.streams)
             if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
                 return VC3_ERR_CUDA;
+        {
+            int prev = 0;
+            cudaGetDevice(&prev);
+            const bool ok = cudaSetDevice(device) == cudaSuccess &&
+                            cudaMalloc((void**)&c.d_bad, sizeof(int32_t)) == cudaSuccess;
+            cudaSetDevice(prev);
+            if (!ok) return VC3_ERR_CUDA;
+        }
         c.ready = true;
     }
     *out = &c;
@@ -80,6 +90,7 @@ int pipeline(const void* const (&in)[NIN], const int (&in_bytes)[NIN], void* out
     DeviceCtx* ctx = nullptr;
     int st = ctx_for(device, &ctx);
     if (st) return st;
+    std::lock_guard<std::recursive_mutex> call_lock(ctx->call_mu);
     const int64_t chunk = std::min(n, kChunk);
     const int nbuf = (int)std::min<int64_t>(kStreams, (n + chunk - 1) / chunk);
     char* dev_in[kStreams][NIN] = {};
@@ -139,25 +150,33 @@ int vc3_compress_host(const float* xyz_host, uint64_t* words_host, int64_t n, vc
     if (policy > 7u || (n > 0 && (!xyz_host || !words_host))) return VC3_ERR_ARG;
     if (nonfinite_out) *nonfinite_out = 0;
     if (n == 0) return VC3_OK;
-    int32_t* d_bad = nullptr;
+    DeviceCtx* ctx = nullptr;
+    int st = ctx_for(device, &ctx);
+    if (st) return st;
+    int32_t* d_bad = ctx->d_bad;
+    std::lock_guard<std::recursive_mutex> call_lock(ctx->call_mu);  // held across the pipeline
     {
+        // zeroed and synchronised before any pipeline stream touches it
         DeviceGuard guard(device);
-        if (!guard.ok || cudaMalloc((void**)&d_bad, sizeof(int32_t)) != cudaSuccess ||
-            cudaMemset(d_bad, 0, sizeof(int32_t)) != cudaSuccess)
+        if (!guard.ok || cudaMemsetAsync(d_bad, 0, sizeof(int32_t), ctx->streams[0]) != cudaSuccess ||
+            cudaStreamSynchronize(ctx->streams[0]) != cudaSuccess)
             return VC3_ERR_CUDA;
     }
     const void* const in[1] = {xyz_host};
     const int bytes[1] = {12};
-    int st = pipeline<1>(in, bytes, words_host, 8, n, device,
-                         [&](const void* const* d, void* o, int64_t cnt, cudaStream_t s) {
-                             return vc3_compress((const float*)d[0], (uint64_t*)o, cnt, layout,
-                                                 policy, d_bad, s);
-                         });
+    st = pipeline<1>(in, bytes, words_host, 8, n, device,
+                     [&](const void* const* d, void* o, int64_t cnt, cudaStream_t s) {
+                         return vc3_compress((const float*)d[0], (uint64_t*)o, cnt, layout, policy,
+                                             d_bad, s);
+                     });
+    // the pipeline synchronised its streams: the count is final
     DeviceGuard guard(device);
     int32_t bad = 0;
-    if (cudaMemcpy(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess && !st)
-        st = VC3_ERR_CUDA;
-    cudaFree(d_bad);
+    if (cudaMemcpyAsync(&bad, d_bad, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->streams[0]) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(ctx->streams[0]) != cudaSuccess) {
+        if (!st) st = VC3_ERR_CUDA;
+    }
     if (nonfinite_out) *nonfinite_out = bad;
     if (!st && bad > 0) st = VC3_ERR_NONFINITE;
     return st;

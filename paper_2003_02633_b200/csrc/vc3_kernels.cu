@@ -142,17 +142,43 @@ struct TableKey {
 std::mutex g_tab_mu;
 std::map<TableKey, double2*> g_tabs;
 
-int get_table(const Params& P, const double2** out) {
+// Upload a host table into fresh device memory, safe on first use inside a
+// caller's CUDA-graph capture and independent of the caller's stream: the
+// thread switches to relaxed capture mode for the allocation, and the copy
+// runs on a library-private non-blocking stream that is synchronised before
+// returning (so no later kernel on any stream can see the memory early).
+int upload_table(const void* h, size_t bytes, double2** out) {
     *out = nullptr;
-    if (!P.table_mode) return VC3_OK;
-    const TableKey key{current_device(), P.t, P.p};
-    std::lock_guard<std::mutex> lock(g_tab_mu);
-    auto it = g_tabs.find(key);
-    if (it != g_tabs.end()) {
-        *out = it->second;
-        return VC3_OK;
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    static std::mutex smu;
+    static std::map<int, cudaStream_t> streams;
+    cudaStream_t s = nullptr;
+    int st = VC3_OK;
+    {
+        std::lock_guard<std::mutex> lock(smu);
+        const int dev = current_device();
+        auto it = streams.find(dev);
+        if (it == streams.end()) {
+            st = cuda_status(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            if (!st) streams[dev] = s;
+        } else {
+            s = it->second;
+        }
     }
-    // layout: [theta grid (t_n - 1)][theta endpoint nt = ntmax][phi grid (p_n - 1)][phi pole]
+    double2* d = nullptr;
+    if (!st) st = cuda_status(cudaMalloc((void**)&d, bytes));
+    if (!st) st = cuda_status(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s));
+    if (!st) st = cuda_status(cudaStreamSynchronize(s));
+    if (st && d) cudaFree(d);
+    cudaThreadExchangeStreamCaptureMode(&mode);  // restore the caller's mode
+    if (!st) *out = d;
+    return st;
+}
+
+// layout of the fast table: [theta grid (t_n - 1)][theta endpoint nt = ntmax]
+// [phi grid (p_n - 1)][phi pole]
+std::vector<double2> fast_table_host(const Params& P) {
     std::vector<double2> h((size_t)P.tab_n);
     for (int i = 0; i < P.t_n - 1; ++i) {
         double s, c;
@@ -166,14 +192,22 @@ int get_table(const Params& P, const double2** out) {
         h[P.p_base + i] = make_double2(s, c);
     }
     h[P.p_base + P.p_n - 1] = make_double2(0.0, -1.0);  // nph = npmax: the reference's exact pole
-    double2* d = nullptr;
-    int st = cuda_status(cudaMalloc((void**)&d, h.size() * sizeof(double2)));
-    if (st) return st;
-    st = cuda_status(cudaMemcpy(d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
-    if (st) {
-        cudaFree(d);
-        return st;
+    return h;
+}
+
+int get_table(const Params& P, const double2** out) {
+    *out = nullptr;
+    if (!P.table_mode) return VC3_OK;
+    const TableKey key{current_device(), P.t, P.p};
+    std::lock_guard<std::mutex> lock(g_tab_mu);
+    auto it = g_tabs.find(key);
+    if (it != g_tabs.end()) {
+        *out = it->second;
+        return VC3_OK;
     }
+    const std::vector<double2> h = fast_table_host(P);
+    double2* d = nullptr;
+    if (const int st = upload_table(h.data(), h.size() * sizeof(double2), &d)) return st;
     g_tabs[key] = d;
     *out = d;
     return VC3_OK;
@@ -182,35 +216,23 @@ int get_table(const Params& P, const double2** out) {
 // The reference's own decode tables (_kernels.py:252-273): glibc sin/cos of
 // th = _PI*(2n/ntmax - 1) and ph = _PI*n/npmax, exact pole; 6 MB at the
 // default layout, device-resident, read only for the rare boundary cases of
-// the bit-identical decompress.
+// the bit-identical decodes.
 std::map<TableKey, double2*> g_full;
+std::map<TableKey, double> g_tol;
 
-// Largest |fast table sin/cos - reference sin/cos| over every theta index
-// (err[0]) and every phi index (err[1]), as decompress_one indexes the table.
-__global__ void k_table_err(const double2* __restrict__ tab, const double2* __restrict__ full,
-                            Params P, unsigned long long* err) {
-    const long long nT = P.ntmax + 1, nP = P.npmax + 1;
-    double et = 0.0, ep = 0.0;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nT + nP;
-         i += (long long)gridDim.x * blockDim.x) {
-        double s, c;
-        const double2 A = full[i];
-        if (i < nT) {
-            const int nt = (int)i;
-            const bool endp = nt == (int)P.ntmax;
-            sincos_tab(tab, endp ? P.t_n - 1 : nt >> P.t_shift, endp ? 0 : nt & ((1 << P.t_shift) - 1),
-                       P.t_delta, s, c);
-            et = fmax(et, fmax(fabs(s - A.x), fabs(c - A.y)));
-        } else {
-            const int nph = (int)(i - nT);
-            const bool pole = nph == (int)P.npmax;
-            sincos_tab(tab + P.p_base, pole ? P.p_n - 1 : nph >> P.p_shift,
-                       pole ? 0 : nph & ((1 << P.p_shift) - 1), P.p_delta, s, c);
-            ep = fmax(ep, fmax(fabs(s - A.x), fabs(c - A.y)));
-        }
-    }
-    atomicMax(err, (unsigned long long)__double_as_longlong(et));
-    atomicMax(err + 1, (unsigned long long)__double_as_longlong(ep));
+// The device's table + residual evaluation (sincos_resid, vc3_device.cuh)
+// restated on the host: every step is one IEEE double operation (std::fma is
+// correctly rounded; the host build has no FMA contraction), so the results
+// are the device's bit for bit.
+void sincos_resid_host(double2 A, int lo, double delta, double* s, double* c) {
+    const double psi = std::fma((double)(4503599627370496LL + lo), delta, -4503599627370496.0 * delta);
+    const volatile double u = psi * psi;
+    const volatile double pu = psi * u;
+    const double sps = std::fma(pu, -1.0 / 6.0, psi);
+    const volatile double cq = std::fma(u, 1.0 / 24.0, -0.5);
+    const volatile double cm1 = u * cq;
+    *s = std::fma(A.y, sps, std::fma(A.x, cm1, A.x));
+    *c = std::fma(-A.x, sps, std::fma(A.y, cm1, A.y));
 }
 
 // Decode tolerance (relative to r): a decoded component fl(fl(r*c')*s') vs
@@ -243,32 +265,38 @@ int get_full_table(const Params& P, const double2** out) {
         h[(size_t)(P.ntmax + 1 + n)] = make_double2(std::sin(ph), std::cos(ph));
     }
     h[(size_t)(P.ntmax + 1 + P.npmax)] = make_double2(0.0, -1.0);
+    // largest |fast table sin/cos - reference sin/cos| over every theta index
+    // (et) and every phi index (ep), indexed as the decodes index the table
+    const std::vector<double2> fast = fast_table_host(P);
+    double et = 0.0, ep = 0.0;
+    for (long long nt = 0; nt <= P.ntmax; ++nt) {
+        const long long b = nt + (nt == P.ntmax ? 1 : 0);
+        double s, c;
+        sincos_resid_host(fast[(size_t)(b >> P.t_shift)], (int)(b & ((1 << P.t_shift) - 1)), P.t_delta, &s, &c);
+        et = std::fmax(et, std::fmax(std::fabs(s - h[(size_t)nt].x), std::fabs(c - h[(size_t)nt].y)));
+    }
+    for (long long nph = 0; nph <= P.npmax; ++nph) {
+        const long long b = nph + (nph == P.npmax ? 1 : 0);
+        double s, c;
+        sincos_resid_host(fast[(size_t)(P.p_base + (b >> P.p_shift))], (int)(b & ((1 << P.p_shift) - 1)),
+                          P.p_delta, &s, &c);
+        const double2 R = h[(size_t)(P.ntmax + 1 + nph)];
+        ep = std::fmax(ep, std::fmax(std::fabs(s - R.x), std::fabs(c - R.y)));
+    }
+    const double tol = decode_tolerance(et, ep);
+    h.back() = make_double2(tol, 0.0);
     double2* d = nullptr;
-    int st = cuda_status(cudaMalloc((void**)&d, h.size() * sizeof(double2) + 16));
-    if (st) return st;
-    unsigned long long* err = (unsigned long long*)(d + h.size());
-    st = cuda_status(cudaMemcpy(d, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
-    if (!st) st = cuda_status(cudaMemset(err, 0, 16));
-    if (!st) {
-        k_table_err<<<2 * 148, 256>>>(seed, d, P, err);
-        st = cuda_status(cudaGetLastError());
-    }
-    unsigned long long e2[2] = {0, 0};
-    if (!st) st = cuda_status(cudaMemcpy(e2, err, 16, cudaMemcpyDeviceToHost));
-    if (!st) {
-        double et, ep;
-        std::memcpy(&et, &e2[0], 8);
-        std::memcpy(&ep, &e2[1], 8);
-        h.back() = make_double2(decode_tolerance(et, ep), 0.0);
-        st = cuda_status(cudaMemcpy(d + h.size() - 1, &h.back(), sizeof(double2), cudaMemcpyHostToDevice));
-    }
-    if (st) {
-        cudaFree(d);
-        return st;
-    }
+    if (const int st = upload_table(h.data(), h.size() * sizeof(double2), &d)) return st;
     g_full[key] = d;
+    g_tol[key] = tol;
     *out = d;
     return VC3_OK;
+}
+
+double full_table_tolerance(const Params& P) {
+    std::lock_guard<std::mutex> lock(g_tab_mu);
+    auto it = g_tol.find(TableKey{current_device(), P.t, P.p});
+    return it == g_tol.end() ? 0.0 : it->second;
 }
 
 size_t table_smem(const Params& P) { return P.table_mode ? (size_t)P.tab_n * sizeof(double2) : 0; }
@@ -536,10 +564,14 @@ __global__ void __launch_bounds__(kThreads) k_decode_mag(const long long* __rest
 
 __global__ void __launch_bounds__(kThreads) k_mag_events(const float* __restrict__ xyz, int64_t n,
                                                          Params P,
-                                                         unsigned long long* __restrict__ counts) {
+                                                         unsigned long long* __restrict__ counts,
+                                                         int32_t* __restrict__ nonfinite) {
     unsigned long long fl = 0, sat = 0;
+    int bad = 0;
     for (int64_t i = gtid(); i < n; i += gstride()) {
-        const double xd = xyz[3 * i], yd = xyz[3 * i + 1], zd = xyz[3 * i + 2];
+        const float x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+        bad += !finite3(x, y, z);
+        const double xd = x, yd = y, zd = z;
         const double r = __dsqrt_rn(__fma_rn(zd, zd, __fma_rn(yd, yd, __dmul_rn(xd, xd))));
         if (r > 0.0) {
             const unsigned u = __float_as_uint(__double2float_ru(r));
@@ -550,6 +582,7 @@ __global__ void __launch_bounds__(kThreads) k_mag_events(const float* __restrict
     }
     if (fl) atomicAdd(counts, fl);
     if (sat) atomicAdd(counts + 1, sat);
+    if (bad && nonfinite) atomicAdd(nonfinite, bad);
 }
 
 // ----- K6 error statistics (analysis.py:118-167) ------------------------------
@@ -740,13 +773,23 @@ int vc3_decode_tolerance(vc3_layout layout, double* tol) {
     const Params P = make_params(layout);
     *tol = 0.0;
     const double2* full = nullptr;
-    int st = get_full_table(P, &full);
+    const int st = get_full_table(P, &full);
     if (st || !full) return st;
-    double2 last;
-    st = cuda_status(cudaMemcpy(&last, full + (P.ntmax + 1) + (P.npmax + 1), sizeof(last),
-                                cudaMemcpyDeviceToHost));
-    if (!st) *tol = last.x;
-    return st;
+    *tol = full_table_tolerance(P);
+    return VC3_OK;
+}
+
+int vc3_prepare_layout(vc3_layout layout, uint32_t flags) {
+    if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
+    if (flags & ~VC3_FLAGS_ALL) return VC3_ERR_ARG;
+    const Params P = make_params(layout);
+    const double2* tab = nullptr;
+    if (const int st = get_table(P, &tab)) return st;
+    if (!(flags & VC3_CONTRACT)) {
+        const double2* full = nullptr;
+        if (const int st = get_full_table(P, &full)) return st;
+    }
+    return VC3_OK;
 }
 
 int vc3_decompress_ex(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout,
@@ -864,13 +907,44 @@ int vc3_decode_magnitude(const int64_t* field, float* r, int64_t n, vc3_layout l
     return launch_status();
 }
 
-int vc3_magnitude_events(const float* xyz, int64_t n, vc3_layout layout,
-                         unsigned long long* d_counts, void* stream) {
+int vc3_magnitude_events_checked(const float* xyz, int64_t n, vc3_layout layout,
+                                 unsigned long long* d_counts, int32_t* d_nonfinite, void* stream) {
     if (!layout_ok(layout)) return VC3_ERR_LAYOUT;
     VC3_CHECK_N(n);
     if (!xyz || !d_counts) return VC3_ERR_ARG;
     k_mag_events<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(xyz, n, make_params(layout),
-                                                                    d_counts);
+                                                                    d_counts, d_nonfinite);
+    return launch_status();
+}
+
+int vc3_magnitude_events(const float* xyz, int64_t n, vc3_layout layout,
+                         unsigned long long* d_counts, void* stream) {
+    return vc3_magnitude_events_checked(xyz, n, layout, d_counts, nullptr, stream);
+}
+
+int vc3_error_stats_workspace(int64_t n, int64_t chunk, uint64_t* bytes) {
+    if (n < 0 || chunk <= 0 || !bytes) return VC3_ERR_ARG;
+    const int64_t nchunks = n ? (n + chunk - 1) / chunk : 0;
+    const int64_t slices = n ? (std::min(chunk, n) + kStatSlice - 1) / kStatSlice : 0;
+    *bytes = (uint64_t)(sizeof(Moments) * slices * nchunks);
+    return VC3_OK;
+}
+
+int vc3_error_stats_ws(const float* v, const float* vh, int64_t n, int32_t kind, int64_t chunk,
+                       double* d_chunk_stats, void* d_work, uint64_t work_bytes, void* stream) {
+    if (kind < VC3_ERR_L2 || kind > VC3_ERR_REL_MAGNITUDE) return VC3_ERR_ARG;
+    VC3_CHECK_N(n);
+    if (!v || !vh || !d_chunk_stats || chunk <= 0) return VC3_ERR_ARG;
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    const int64_t slices64 = (std::min(chunk, n) + kStatSlice - 1) / kStatSlice;
+    if (slices64 > 65535 || nchunks > 65535) return VC3_ERR_ARG;
+    if (!d_work || work_bytes < sizeof(Moments) * slices64 * nchunks) return VC3_ERR_ARG;
+    const int slices = (int)slices64;
+    cudaStream_t s = (cudaStream_t)stream;
+    Moments* part = (Moments*)d_work;
+    k_err_partial<<<dim3(slices, (unsigned)nchunks), kStatThreads, 0, s>>>(v, vh, n, kind,
+                                                                          chunk, slices, part);
+    k_err_final<<<grid_for(nchunks), kThreads, 0, s>>>(part, nchunks, slices, d_chunk_stats);
     return launch_status();
 }
 
@@ -879,18 +953,15 @@ int vc3_error_stats(const float* v, const float* vh, int64_t n, int32_t kind, in
     if (kind < VC3_ERR_L2 || kind > VC3_ERR_REL_MAGNITUDE) return VC3_ERR_ARG;
     VC3_CHECK_N(n);
     if (!v || !vh || !d_chunk_stats || chunk <= 0) return VC3_ERR_ARG;
-    const int64_t nchunks = (n + chunk - 1) / chunk;
-    const int64_t slices64 = (std::min(chunk, n) + kStatSlice - 1) / kStatSlice;
-    if (slices64 > 65535 || nchunks > 65535) return VC3_ERR_ARG;
-    const int slices = (int)slices64;
+    uint64_t bytes = 0;
+    vc3_error_stats_workspace(n, chunk, &bytes);
     cudaStream_t s = (cudaStream_t)stream;
-    Moments* part = nullptr;
-    int st = cuda_status(cudaMallocAsync((void**)&part, sizeof(Moments) * slices * nchunks, s));
+    // stream-ordered scratch from the device's default memory pool (no
+    // device-wide synchronisation; legal inside graph capture)
+    void* part = nullptr;
+    int st = cuda_status(cudaMallocAsync(&part, bytes, s));
     if (st) return st;
-    k_err_partial<<<dim3(slices, (unsigned)nchunks), kStatThreads, 0, s>>>(v, vh, n, kind,
-                                                                          chunk, slices, part);
-    k_err_final<<<grid_for(nchunks), kThreads, 0, s>>>(part, nchunks, slices, d_chunk_stats);
-    st = launch_status();
+    st = vc3_error_stats_ws(v, vh, n, kind, chunk, d_chunk_stats, part, bytes, stream);
     cudaFreeAsync(part, s);
     return st;
 }

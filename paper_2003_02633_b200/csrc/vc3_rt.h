@@ -23,6 +23,7 @@ bool is_default_layout(const vc3_layout& L);
 int get_table(const Params& P, const double2** out);  // nullptr when !P.table_mode
 // the reference's own decode tables + the measured decode tolerance (exact modes)
 int get_full_table(const Params& P, const double2** out);
+double full_table_tolerance(const Params& P);  // host copy of the measured tolerance
 size_t table_smem(const Params& P);
 int ensure_smem(const void* func, size_t bytes);       // opt in to > 48 KB dynamic smem
 
