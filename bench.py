@@ -195,7 +195,7 @@ def run_reference(args, world, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": workload_config(N_PER_GPU, world),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", **host_info(),
                          "sample": f"{sample} cube vectors per step (bounded sample of the "
                                    f"2^28-vector workload), oracle/vc3_oracle.c add_compressed "
                                    f"on {threads} host threads"},
@@ -225,9 +225,82 @@ def cpu_baseline_sample(sample: int = CPU_SAMPLE) -> dict:
     for _ in range(reps):
         vc3_oracle.add_compressed(a, b, DEFAULT_LAYOUT, ALL_SINGLE_POLICY, threads)
     dt = (time.perf_counter() - t0) / reps
-    return {"value": sample / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{reps} x {sample} cube vectors, oracle/vc3_oracle.c add_compressed, "
-                      f"{threads} threads, after 1 warm-up pass"}
+    out = {"value": sample / dt / 1e9, "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"{reps} x {sample} cube vectors, oracle/vc3_oracle.c add_compressed, "
+                     f"{threads} threads, after 1 warm-up pass"}
+    out.update(host_info())
+    shipped = numba_reference_sample(a, b)
+    if shipped is not None:
+        out["reference_as_shipped"] = shipped
+    return out
+
+
+def host_info() -> dict:
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(),
+            "affinity_cores": len(os.sched_getaffinity(0))}
+
+
+_NB_OPERANDS = None  # (a, b) inherited by the fork pool's workers (never pickled)
+
+
+def _numba_shard(bounds):
+    """Worker of the fork pool: the reference's own add_compressed on one
+    contiguous shard (inputs inherited through fork, result discarded)."""
+    import vc3.bench as rb
+
+    lo, hi = bounds
+    a, b = _NB_OPERANDS
+    t0 = time.perf_counter()
+    rb.add_compressed(a[lo:hi], b[lo:hi])
+    return time.perf_counter() - t0
+
+
+def numba_reference_sample(a: np.ndarray, b: np.ndarray) -> dict | None:
+    """The reference's shipped CPU path (numba kernels through
+    vc3.bench.add_compressed, bench.py:41-69), installed offline into
+    baseline/_ref: one core as shipped, then sharded over all cores with a
+    fork process pool.  None when it is not installed."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "vc3").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/vc3_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import vc3.bench as rb
+    except Exception as exc:  # numba missing or broken: report, do not fail the bench
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+    n = min(a.size, 1 << 21)
+    rb.add_compressed(a[:1024], b[:1024])  # JIT compile (cached)
+    t0 = time.perf_counter()
+    rb.add_compressed(a[:n], b[:n])
+    one = n / (time.perf_counter() - t0) / 1e9
+    import multiprocessing as mp
+
+    global _NB_OPERANDS
+    procs = len(os.sched_getaffinity(0))
+    nn = min(a.size, n * procs)
+    _NB_OPERANDS = (a, b)
+    bounds = [(nn * i // procs, nn * (i + 1) // procs) for i in range(procs)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        pool.map(_numba_shard, [(0, 1024)] * procs, chunksize=1)  # warm every worker's JIT
+        t0 = time.perf_counter()
+        pool.map(_numba_shard, bounds, chunksize=1)
+        allc = nn / (time.perf_counter() - t0) / 1e9
+    _NB_OPERANDS = None
+    return {"one_core": {"value": one, "unit": UNIT, "cores": 1,
+                         "sample": f"{n} cube vectors, vc3.bench.add_compressed (numba, as shipped)"},
+            "all_cores": {"value": allc, "unit": UNIT, "cores": procs,
+                          "sample": f"{nn} vectors in {procs} contiguous shards, fork pool"}}
 
 
 def time_region(fn, steps, stream, torch):
@@ -473,20 +546,21 @@ def run_gpu(args, world, rank, local):
     cl = _native.c_layout(lay)
     sptr = stream.cuda_stream
 
-    def step_add():
-        lib.vc3_add_compressed(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, cl, pol.mask, sptr)
+    def step_add(flags=0, out=None):
+        lib.vc3_add_compressed_ex(a.data_ptr(), b.data_ptr(), (out if out is not None else c).data_ptr(),
+                                  n, cl, pol.mask, flags, sptr)
 
-    rc = lib.vc3_add_compressed(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, cl, pol.mask, sptr)
+    rc = lib.vc3_add_compressed_ex(a.data_ptr(), b.data_ptr(), c.data_ptr(), n, cl, pol.mask, 0, sptr)
     _native.check(rc, "add_compressed")
     for _ in range(args.warmup):
         step_add()
     torch.cuda.synchronize()
 
-    def timed(label_steps):
+    def timed(label_steps, fn=step_add):
         barrier()
         torch.cuda.synchronize()
         with ClockSampler(dev.index) as clk:
-            ms = time_region(step_add, label_steps, stream, torch)
+            ms = time_region(fn, label_steps, stream, torch)
         torch.cuda.synchronize()
         barrier()
         return ms, clk.summary()
@@ -499,6 +573,16 @@ def run_gpu(args, world, rank, local):
         remeasured = True
     ms_all = max_over_ranks(ms)
     value = global_n / (ms_all * 1e-3) / 1e9
+
+    # the north-star tolerance mode (VC3_CONTRACT) on the same operands
+    c_ct = torch.empty_like(a)
+    step_ct = lambda: step_add(1, c_ct)
+    for _ in range(args.warmup):
+        step_ct()
+    ms_ct, clocks_ct = timed(args.steps, step_ct)
+    ms_ct_all = max_over_ranks(ms_ct)
+    value_ct = global_n / (ms_ct_all * 1e-3) / 1e9
+    step_add()  # c = the exact words again
 
     # uncompressed float32 baseline on the same GPU (same vectors, 36 B/vec)
     ra = va.reshape(-1)
@@ -515,57 +599,88 @@ def run_gpu(args, world, rank, local):
     raw_ms = max_over_ranks(time_region(step_raw, args.steps, stream, torch))
     raw_value = global_n / (raw_ms * 1e-3) / 1e9
 
-    # secondary kernels (compress / decompress) for the roofline table
+    # secondary kernels: compress, decompress (both modes) and the fused axpy
+    # y' = 0.75 x + y (24 B/vector, both modes), each with its roofline
+    peak, peak_src = measured_peak()
     out_v = torch.empty_like(va)
+    y_out = torch.empty_like(a)
 
-    def step_comp():
-        lib.vc3_compress(va.data_ptr(), c.data_ptr(), n, cl, pol.mask, None, sptr)
-
-    def step_decomp():
-        lib.vc3_decompress(a.data_ptr(), out_v.data_ptr(), n, cl, sptr)
+    def kline(t_ms, nbytes):
+        gbs = nbytes * n / (t_ms * 1e-3) / 1e9
+        return {"gvec_s": n / (t_ms * 1e-3) / 1e9, "gb_s": gbs, "frac_of_peak": gbs / peak, "ms": t_ms}
 
     sec = {}
-    for name, fn in (("compress", step_comp), ("decompress", step_decomp)):
+    for name, fn, nbytes in (
+            ("compress", lambda: lib.vc3_compress(va.data_ptr(), c.data_ptr(), n, cl, pol.mask, None, sptr), 20),
+            ("decompress_exact", lambda: lib.vc3_decompress_ex(a.data_ptr(), out_v.data_ptr(), n, cl, 0, sptr), 20),
+            ("decompress_contract", lambda: lib.vc3_decompress_ex(a.data_ptr(), out_v.data_ptr(), n, cl, 1, sptr), 20),
+            ("axpy_exact", lambda: lib.vc3_axpy_ex(0.75, a.data_ptr(), b.data_ptr(), y_out.data_ptr(), n, cl,
+                                                   pol.mask, 0, sptr), 24),
+            ("axpy_contract", lambda: lib.vc3_axpy_ex(0.75, a.data_ptr(), b.data_ptr(), y_out.data_ptr(), n, cl,
+                                                      pol.mask, 1, sptr), 24)):
         fn()
         torch.cuda.synchronize()
-        t = time_region(fn, max(3, args.steps // 10), stream, torch)
-        sec[name] = {"gvec_s": n / (t * 1e-3) / 1e9, "gb_s": 20 * n / (t * 1e-3) / 1e9, "ms": t}
-    del out_v
+        sec[name] = kline(time_region(fn, max(3, args.steps // 5), stream, torch), nbytes)
+    del out_v, y_out
+    step_add()  # c was reused by the compress timing
 
-    # e2e: public host-array API, pinned host buffers, copies inside the region
-    # pinned host staging: one 2^28 shard (6 GiB) at N = 1; a quarter of that
-    # per rank under torchrun so eight ranks pin 12 GiB, not 48
+    # parity at scale, in the measured run: the first 2^24 pairs of the timed
+    # operands against the CPU oracle (C restatement of the reference path);
+    # exact mode must match bit for bit, contract-mode differences are the ties
+    parity = None
+    if rank == 0:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import vc3_oracle
+
+        ns = min(n, 1 << 24)
+        ha_s, hb_s = a[:ns].cpu().numpy(), b[:ns].cpu().numpy()
+        want = vc3_oracle.add_compressed(ha_s, hb_s, lay, pol, vc3_oracle.default_threads())
+        got_ex, got_ct = c[:ns].cpu().numpy(), c_ct[:ns].cpu().numpy()
+        parity = {"n_pairs": ns, "oracle": "oracle/vc3_oracle.c add_compressed (CPU)",
+                  "exact_mismatches": int((got_ex != want).sum()),
+                  "contract_ties": tie_stats(got_ct, want, lay)}
+    del c_ct
+
+    # e2e: public host-array API with the host<->device copies in the timed
+    # region, from pinned buffers and from plain (pageable) numpy arrays; one
+    # 2^28 shard at N = 1, a quarter of that per rank under torchrun
     e2e_n = min(n, N_PER_GPU if world == 1 else N_PER_GPU // 4)
-    ha = torch.empty(e2e_n, dtype=torch.uint64, pin_memory=True)
-    hb = torch.empty(e2e_n, dtype=torch.uint64, pin_memory=True)
-    ha.copy_(a[:e2e_n])
-    hb.copy_(b[:e2e_n])
-    na, nb = ha.numpy(), hb.numpy()
-    hc = torch.empty(e2e_n, dtype=torch.uint64, pin_memory=True).numpy()
     e2e_steps = max(1, min(args.steps, 5))
+    pinned = [torch.empty(e2e_n, dtype=torch.uint64, pin_memory=True) for _ in range(3)]
+    pinned[0].copy_(a[:e2e_n])
+    pinned[1].copy_(b[:e2e_n])
+    pin_np = [t.numpy() for t in pinned]
+    page_np = [np.empty(e2e_n, dtype=np.uint64) for _ in range(3)]
+    page_np[0][:] = pin_np[0]
+    page_np[1][:] = pin_np[1]
 
-    def step_e2e():
-        rc2 = lib.vc3_add_compressed_host(na.ctypes.data, nb.ctypes.data, hc.ctypes.data, e2e_n,
-                                          cl, pol.mask, dev.index)
-        _native.check(rc2, "add_compressed_host")
+    def e2e_time(bufs):
+        def step():
+            rc2 = lib.vc3_add_compressed_host(bufs[0].ctypes.data, bufs[1].ctypes.data, bufs[2].ctypes.data,
+                                              e2e_n, cl, pol.mask, dev.index)
+            _native.check(rc2, "add_compressed_host")
+        step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            step()
+        return max_over_ranks((time.perf_counter() - t0) / e2e_steps)
 
-    step_e2e()
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        step_e2e()
-    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+    e2e_s = e2e_time(pin_np)
+    e2e_page_s = e2e_time(page_np)
     e2e_value = e2e_n * world / e2e_s / 1e9
-    step_add()  # c was reused by the compress timing; recompute and cross-check e2e output
-    if not np.array_equal(hc, c[:e2e_n].cpu().numpy()):
+    e2e_page_value = e2e_n * world / e2e_page_s / 1e9
+    ref_c = c[:e2e_n].cpu().numpy()
+    if not (np.array_equal(pin_np[2], ref_c) and np.array_equal(page_np[2], ref_c)):
         raise RuntimeError("host-API result differs from the device kernel result")
+    del pinned, pin_np, page_np
 
     # secondary configs are single-GPU characterisations; scaling runs skip them
     secondary_configs = ({} if (args.no_secondary or world > 1)
                          else run_secondary(args, vc3b, lib, dev, stream, min(n, N_PER_GPU)))
 
-    peak, peak_src = measured_peak()
     achieved = BYTES_COMPRESSED * n / (ms * 1e-3) / 1e9
+    achieved_ct = BYTES_COMPRESSED * n / (ms_ct * 1e-3) / 1e9
     traffic = ncu_traffic()
     if rank != 0:
         return
@@ -575,14 +690,25 @@ def run_gpu(args, world, rank, local):
         "warmup": args.warmup, "ms_per_step": ms_all, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(n, world, args.scaling, global_n),
+        "mode": "exact (VC3_EXACT: output words bit-identical to the reference)",
         "hbm_gb_s": BYTES_COMPRESSED * global_n / (ms_all * 1e-3) / 1e9,
+        "contract_mode": {
+            "value": value_ct, "unit": UNIT, "ms_per_step": ms_ct_all,
+            "hbm_gb_s": BYTES_COMPRESSED * global_n / (ms_ct_all * 1e-3) / 1e9,
+            "roofline_frac": achieved_ct / peak,
+            "speedup_vs_fp32_add": value_ct / raw_value,
+            "ties": parity["contract_ties"] if parity else None,
+            "clocks": {k: clocks_ct[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
+            "definition": "VC3_CONTRACT: BASELINE.json north-star tolerance (decoded components "
+                          "within 1 ulp of the reference decode, words bit-exact except one-bin ties)"},
+        "parity_vs_oracle": parity,
         "fp32_add": {"value": raw_value, "unit": UNIT,
                      "hbm_gb_s": BYTES_RAW * global_n / (raw_ms * 1e-3) / 1e9,
                      "ms_per_step": raw_ms},
         "speedup_vs_fp32_add": value / raw_value,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "kernel": "k_add<7,true> (fused decompress-add-recompress)",
+                     "kernel": "k_add_as<exact, default layout> (fused decompress-add-recompress)",
                      "algorithmic_bytes_per_launch": BYTES_COMPRESSED * n},
         "secondary_kernels": sec,
         "secondary_configs": secondary_configs,
@@ -590,6 +716,9 @@ def run_gpu(args, world, rank, local):
                 "d2h_bytes_per_step": 8 * e2e_n,
                 "path": "vc3_add_compressed_host (C ABI; paper_2003_02633_b200.add_compressed "
                         "on numpy arrays), pinned host buffers, chunked H2D/kernel/D2H overlap",
+                "pageable": {"value": e2e_page_value, "unit": UNIT,
+                             "frac_of_pinned": e2e_page_value / e2e_value,
+                             "path": "the same call on plain numpy (pageable) arrays"},
                 "steps": e2e_steps},
         "gpu_launches": args.steps,
         "clocks": {k: clocks[k] for k in ("sm_mhz", "sm_max_mhz", "reasons")},
@@ -599,6 +728,25 @@ def run_gpu(args, world, rank, local):
     if cpu is not None:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
+
+
+def tie_stats(got: np.ndarray, want: np.ndarray, lay) -> dict:
+    """Words that differ from the oracle's: rate and the largest bucket /
+    field deltas (theta wraps at +-pi)."""
+    d = got != want
+    t, p = lay.theta_bits, lay.phi_bits
+    g, w = got[d].astype(np.int64), want[d].astype(np.int64)
+    out = {"n": int(d.size), "n_diff": int(d.sum()), "rate": float(d.mean())}
+    if d.any():
+        tm, pm = (1 << t) - 1, (1 << p) - 1
+        dt = np.abs((g & tm) - (w & tm))
+        dt = np.minimum(dt, tm + 1 - dt)
+        out.update(max_dn_theta=int(dt.max()),
+                   max_dn_phi=int(np.abs(((g >> t) & pm) - ((w >> t) & pm)).max()),
+                   max_dfield=int(np.abs((g >> (t + p)) - (w >> (t + p))).max()))
+    else:
+        out.update(max_dn_theta=0, max_dn_phi=0, max_dfield=0)
+    return out
 
 
 def main():

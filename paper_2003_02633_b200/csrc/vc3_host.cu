@@ -7,11 +7,23 @@
 // k and the device->host copy of chunk k-1 overlap (separate copy engines).
 // Device staging comes from a library-private stream-ordered memory pool that
 // keeps its memory between calls, so repeated calls do not pay cudaMalloc.
+//
+// Pageable host buffers (plain numpy arrays, the reference's callers) cannot
+// be DMA'd directly: the driver would stage them one piece at a time on one
+// CPU thread.  For those the pipeline stages through its own pinned ring
+// (kept between calls): a pool of host threads copies chunk k + 1 into, and
+// chunk k - 2 out of, pinned buffers while the copy engines and the kernel
+// work on the chunks in between.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
 #include <cstdint>
+#include <cstring>
+#include <functional>
 #include <mutex>
+#include <thread>
+#include <vector>
 
 #include "../../include/vc3_b200.h"
 
@@ -26,9 +38,82 @@ namespace {
 constexpr int kStreams = VC3_HOST_STREAMS;
 constexpr int64_t kChunk = int64_t(1) << VC3_HOST_CHUNK_LOG2;  // vectors per chunk (2^23: 64 MiB of words)
 
+#ifndef VC3_HOST_STAGE_CHUNK_LOG2
+#define VC3_HOST_STAGE_CHUNK_LOG2 21
+#endif
+constexpr int64_t kStageChunk = int64_t(1) << VC3_HOST_STAGE_CHUNK_LOG2;  // vectors per staged chunk
+constexpr int kMaxIo = 3;  // host operands + result per call
+#ifndef VC3_HOST_COPY_THREADS
+#define VC3_HOST_COPY_THREADS 16u  // staging memcpy threads (capped by the host's cores)
+#endif
+
+// A small pool of host threads for the staging copies (memcpy into / out of
+// the pinned ring): one memcpy thread reaches ~10 GB/s, PCIe 5 ~55 GB/s.
+class CopyPool {
+  public:
+    static CopyPool& get() {
+        // never destroyed: its workers stay blocked on the condition variable
+        // until the process exits (a static object's destructor would tear
+        // the mutex down under them at exit)
+        static CopyPool* pool = new CopyPool();
+        return *pool;
+    }
+    // copy `bytes` in `nthreads_` slices; returns when all slices are done
+    void copy(void* dst, const void* src, size_t bytes) {
+        const int parts = (int)std::max<size_t>(1, std::min<size_t>(workers_.size() + 1, bytes >> 20));
+        const size_t step = (bytes + parts - 1) / parts;
+        {
+            std::lock_guard<std::mutex> lock(mu_);
+            for (int i = 1; i < parts; ++i) {
+                const size_t lo = std::min(bytes, step * i), hi = std::min(bytes, lo + step);
+                if (hi > lo) {
+                    ++pending_;
+                    tasks_.push_back([=] { std::memcpy((char*)dst + lo, (const char*)src + lo, hi - lo); });
+                }
+            }
+        }
+        cv_.notify_all();
+        std::memcpy(dst, src, std::min(bytes, step));  // this thread's slice
+        std::unique_lock<std::mutex> lock(mu_);
+        done_cv_.wait(lock, [&] { return pending_ == 0; });
+    }
+
+  private:
+    CopyPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const unsigned n = std::min(VC3_HOST_COPY_THREADS, std::max(1u, hw)) - 1;
+        for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { run(); });
+        for (auto& t : workers_) t.detach();
+    }
+    void run() {
+        for (;;) {
+            std::function<void()> task;
+            {
+                std::unique_lock<std::mutex> lock(mu_);
+                cv_.wait(lock, [&] { return !tasks_.empty(); });
+                task = std::move(tasks_.back());
+                tasks_.pop_back();
+            }
+            task();
+            {
+                std::lock_guard<std::mutex> lock(mu_);
+                --pending_;
+            }
+            done_cv_.notify_all();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::vector<std::function<void()>> tasks_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    int pending_ = 0;
+};
+
 struct DeviceCtx {
     cudaMemPool_t pool = nullptr;
     cudaStream_t streams[kStreams] = {};
+    char* stage[kStreams][kMaxIo] = {};  // pinned staging ring (pageable callers), grown on demand
+    size_t stage_bytes[kStreams][kMaxIo] = {};
     int32_t* d_bad = nullptr;  // non-finite counter of vc3_compress_host (allocated once)
     std::recursive_mutex call_mu;  // one host-buffer call at a time per device (shared streams)
     bool ready = false;
@@ -77,12 +162,34 @@ struct DeviceGuard {
     ~DeviceGuard() { cudaSetDevice(prev); }
 };
 
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();  // clear: a plain host pointer is not an error
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+int ensure_stage(DeviceCtx* ctx, int slot, int k, size_t bytes) {
+    if (ctx->stage_bytes[slot][k] >= bytes) return VC3_OK;
+    if (ctx->stage[slot][k]) cudaFreeHost(ctx->stage[slot][k]);
+    ctx->stage[slot][k] = nullptr;
+    ctx->stage_bytes[slot][k] = 0;
+    if (cudaHostAlloc((void**)&ctx->stage[slot][k], bytes, cudaHostAllocPortable) != cudaSuccess)
+        return VC3_ERR_CUDA;
+    ctx->stage_bytes[slot][k] = bytes;
+    return VC3_OK;
+}
+
 // Generic chunked pipeline: per chunk, `in_bytes` lists the host inputs'
 // bytes per element, the kernel callback runs on device copies, and one output
-// of `out_bytes` per element comes back.
+// of `out_bytes` per element comes back.  Pinned host buffers are copied
+// directly; pageable ones go through the pinned staging ring.
 template <int NIN, typename Kernel>
 int pipeline(const void* const (&in)[NIN], const int (&in_bytes)[NIN], void* out, int out_bytes,
              int64_t n, int device, Kernel kernel) {
+    static_assert(NIN + 1 <= kMaxIo, "staging ring holds NIN inputs + 1 output");
     if (n < 0) return VC3_ERR_ARG;
     if (n == 0) return VC3_OK;
     DeviceGuard guard(device);
@@ -91,8 +198,11 @@ int pipeline(const void* const (&in)[NIN], const int (&in_bytes)[NIN], void* out
     int st = ctx_for(device, &ctx);
     if (st) return st;
     std::lock_guard<std::recursive_mutex> call_lock(ctx->call_mu);
-    const int64_t chunk = std::min(n, kChunk);
-    const int nbuf = (int)std::min<int64_t>(kStreams, (n + chunk - 1) / chunk);
+    bool staged = !is_pinned(out);
+    for (int i = 0; i < NIN; ++i) staged = staged || !is_pinned(in[i]);
+    const int64_t chunk = std::min(n, staged ? kStageChunk : kChunk);
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    const int nbuf = (int)std::min<int64_t>(kStreams, nchunks);
     char* dev_in[kStreams][NIN] = {};
     char* dev_out[kStreams] = {};
     for (int b = 0; b < nbuf && !st; ++b) {
@@ -103,20 +213,44 @@ int pipeline(const void* const (&in)[NIN], const int (&in_bytes)[NIN], void* out
         if (!st && cudaMallocFromPoolAsync((void**)&dev_out[b], chunk * out_bytes, ctx->pool,
                                            ctx->streams[b]) != cudaSuccess)
             st = VC3_ERR_CUDA;
+        if (staged) {
+            for (int k = 0; k < NIN && !st; ++k) st = ensure_stage(ctx, b, k, chunk * in_bytes[k]);
+            if (!st) st = ensure_stage(ctx, b, NIN, chunk * out_bytes);
+        }
     }
-    for (int64_t off = 0, k = 0; off < n && !st; off += chunk, ++k) {
+    CopyPool& pool = CopyPool::get();
+    // staged: copy a finished chunk's result out of its pinned slot
+    auto retire = [&](int64_t kk) {
+        const int b = (int)(kk % nbuf);
+        const int64_t off = kk * chunk, cnt = std::min(chunk, n - off);
+        if (cudaStreamSynchronize(ctx->streams[b]) != cudaSuccess) return VC3_ERR_CUDA;
+        pool.copy((char*)out + off * out_bytes, ctx->stage[b][NIN], cnt * out_bytes);
+        return VC3_OK;
+    };
+    for (int64_t k = 0; k < nchunks && !st; ++k) {
         const int b = (int)(k % nbuf);
         cudaStream_t s = ctx->streams[b];
-        const int64_t cnt = std::min(chunk, n - off);
-        for (int i = 0; i < NIN; ++i)
-            if (cudaMemcpyAsync(dev_in[b][i], (const char*)in[i] + off * in_bytes[i],
-                                cnt * in_bytes[i], cudaMemcpyHostToDevice, s) != cudaSuccess)
+        const int64_t off = k * chunk, cnt = std::min(chunk, n - off);
+        if (staged && k >= nbuf) st = retire(k - nbuf);  // slot b's previous chunk
+        if (st) break;
+        for (int i = 0; i < NIN; ++i) {
+            const char* src = (const char*)in[i] + off * in_bytes[i];
+            if (staged) {
+                pool.copy(ctx->stage[b][i], src, cnt * in_bytes[i]);
+                src = ctx->stage[b][i];
+            }
+            if (cudaMemcpyAsync(dev_in[b][i], src, cnt * in_bytes[i], cudaMemcpyHostToDevice, s) !=
+                cudaSuccess)
                 st = VC3_ERR_CUDA;
+        }
         if (!st) st = kernel((const void* const*)dev_in[b], (void*)dev_out[b], cnt, s);
-        if (!st && cudaMemcpyAsync((char*)out + off * out_bytes, dev_out[b], cnt * out_bytes,
-                                   cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        char* dst = staged ? ctx->stage[b][NIN] : (char*)out + off * out_bytes;
+        if (!st && cudaMemcpyAsync(dst, dev_out[b], cnt * out_bytes, cudaMemcpyDeviceToHost, s) !=
+                       cudaSuccess)
             st = VC3_ERR_CUDA;
     }
+    if (staged && !st)
+        for (int64_t k = std::max<int64_t>(0, nchunks - nbuf); k < nchunks && !st; ++k) st = retire(k);
     for (int b = 0; b < nbuf; ++b) {
         for (int k = 0; k < NIN; ++k)
             if (dev_in[b][k]) cudaFreeAsync(dev_in[b][k], ctx->streams[b]);
