@@ -192,6 +192,17 @@ std::vector<double2> fast_table_host(const Params& P) {
         h[P.p_base + i] = make_double2(s, c);
     }
     h[P.p_base + P.p_n - 1] = make_double2(0.0, -1.0);  // nph = npmax: the reference's exact pole
+    // residual sections: (sin(l * D), cos(l * D) - 1) for every residual index
+    // l, D = 2 RN(pi) / ntmax (theta) or RN(pi) / npmax (phi), in long double
+    const long double pid = (long double)kPi;
+    for (int l = 0; l < (1 << P.t_shift); ++l) {
+        const long double psi = (long double)l * (2.0L * pid / (long double)P.ntmax);
+        h[P.rt_base + l] = make_double2((double)sinl(psi), (double)(-2.0L * sinl(psi / 2) * sinl(psi / 2)));
+    }
+    for (int l = 0; l < (1 << P.p_shift); ++l) {
+        const long double psi = (long double)l * (pid / (long double)P.npmax);
+        h[P.rp_base + l] = make_double2((double)sinl(psi), (double)(-2.0L * sinl(psi / 2) * sinl(psi / 2)));
+    }
     return h;
 }
 
@@ -235,6 +246,13 @@ void sincos_resid_host(double2 A, int lo, double delta, double* s, double* c) {
     *c = std::fma(-A.x, sps, std::fma(A.y, cm1, A.y));
 }
 
+// The two-level form (decode_fused, vc3_fused.cuh): the residual's
+// (sin psi, cos psi - 1) come from the residual table section.
+void sincos_two_level_host(double2 A, double2 Rs, double* s, double* c) {
+    *s = std::fma(A.y, Rs.x, std::fma(A.x, Rs.y, A.x));
+    *c = std::fma(-A.x, Rs.x, std::fma(A.y, Rs.y, A.y));
+}
+
 // Decode tolerance (relative to r): a decoded component fl(fl(r*c')*s') vs
 // the reference's fl(fl(r*c)*s) with |c - c'| <= et, |s - s'| <= ep differs
 // by at most r*(et + ep + et*ep + 4u(1 + et)(1 + ep)), u = 2^-53; the
@@ -269,19 +287,28 @@ int get_full_table(const Params& P, const double2** out) {
     // (et) and every phi index (ep), indexed as the decodes index the table
     const std::vector<double2> fast = fast_table_host(P);
     double et = 0.0, ep = 0.0;
+    // both decode forms share the tolerance: the residual polynomial
+    // (decompress_one) and the two-level table (decode_fused)
     for (long long nt = 0; nt <= P.ntmax; ++nt) {
         const long long b = nt + (nt == P.ntmax ? 1 : 0);
-        double s, c;
-        sincos_resid_host(fast[(size_t)(b >> P.t_shift)], (int)(b & ((1 << P.t_shift) - 1)), P.t_delta, &s, &c);
-        et = std::fmax(et, std::fmax(std::fabs(s - h[(size_t)nt].x), std::fabs(c - h[(size_t)nt].y)));
+        const int lo = (int)(b & ((1 << P.t_shift) - 1));
+        const double2 A = fast[(size_t)(b >> P.t_shift)], Rf = h[(size_t)nt];
+        double s, c, s2, c2;
+        sincos_resid_host(A, lo, P.t_delta, &s, &c);
+        sincos_two_level_host(A, fast[(size_t)(P.rt_base + lo)], &s2, &c2);
+        et = std::fmax(et, std::fmax(std::fmax(std::fabs(s - Rf.x), std::fabs(c - Rf.y)),
+                                     std::fmax(std::fabs(s2 - Rf.x), std::fabs(c2 - Rf.y))));
     }
     for (long long nph = 0; nph <= P.npmax; ++nph) {
         const long long b = nph + (nph == P.npmax ? 1 : 0);
-        double s, c;
-        sincos_resid_host(fast[(size_t)(P.p_base + (b >> P.p_shift))], (int)(b & ((1 << P.p_shift) - 1)),
-                          P.p_delta, &s, &c);
+        const int lo = (int)(b & ((1 << P.p_shift) - 1));
+        const double2 A = fast[(size_t)(P.p_base + (b >> P.p_shift))];
         const double2 R = h[(size_t)(P.ntmax + 1 + nph)];
-        ep = std::fmax(ep, std::fmax(std::fabs(s - R.x), std::fabs(c - R.y)));
+        double s, c, s2, c2;
+        sincos_resid_host(A, lo, P.p_delta, &s, &c);
+        sincos_two_level_host(A, fast[(size_t)(P.rp_base + lo)], &s2, &c2);
+        ep = std::fmax(ep, std::fmax(std::fmax(std::fabs(s - R.x), std::fabs(c - R.y)),
+                                     std::fmax(std::fabs(s2 - R.x), std::fabs(c2 - R.y))));
     }
     const double tol = decode_tolerance(et, ep);
     h.back() = make_double2(tol, 0.0);
@@ -423,6 +450,7 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const int idx = 32 * k + lane;  // float4 index within the warp's 1536 B
+            VC3_DCHECK(idx < 96 && (threadIdx.x >> 5) * 96 + idx < (blockDim.x >> 5) * 96);
             if (g0 + idx / 3 < groups) {
                 const float4 f = stage[idx];
                 st_f4(base + 4 * idx, f.x, f.y, f.z, f.w);
