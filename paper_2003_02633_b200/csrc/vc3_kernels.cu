@@ -101,6 +101,7 @@ Params make_params(const vc3_layout& L) {
     P.p_delta = (double)(pid / (long double)P.npmax);
     P.t_rcp = 1.0 / (double)P.ntmax;
     P.p_rcp = 1.0 / (double)P.npmax;
+    P.resid_hi = 0x43300000u;
     return P;
 }
 

@@ -121,10 +121,82 @@ __global__ void __launch_bounds__(256, 4) probe_add(const unsigned long long* a,
         }
         unsigned long long w[4];
         bool slow[4];
-        compress_as2(x, y, z, P, w, slow);
-        compress_as2(x + 2, y + 2, z + 2, P, w + 2, slow + 2);
+        compress_as2<true>(x, y, z, P, w, slow);
+        compress_as2<true>(x + 2, y + 2, z + 2, P, w + 2, slow + 2);
         if (__any_sync(__activemask(), slow[0] | slow[1] | slow[2] | slow[3])) w[0] = ~w[0];
         st4(c + 4 * g, w[0], w[1], w[2], w[3]);
+    }
+}
+
+
+// stage probes: each reads four vectors (48 B) and writes four words, so the
+// loop overhead is the same as probe_copy's
+__device__ __forceinline__ void ld12(const float* in, int64_t g, float x[4], float y[4], float z[4]) {
+    const float4* s = reinterpret_cast<const float4*>(in + 12 * g);
+    const float4 A = s[0], B = s[1], C = s[2];
+    x[0] = A.x; y[0] = A.y; z[0] = A.z; x[1] = A.w; y[1] = B.x; z[1] = B.y;
+    x[2] = B.z; y[2] = B.w; z[2] = C.x; x[3] = C.y; y[3] = C.z; z[3] = C.w;
+}
+
+__global__ void __launch_bounds__(256, 3) probe_copy(const float* in, unsigned long long* out, int64_t groups) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
+        float x[4], y[4], z[4];
+        ld12(in, g, x, y, z);
+        unsigned long long w[4];
+        for (int k = 0; k < 4; ++k)
+            w[k] = ((unsigned long long)__float_as_uint(x[k]) << 32) ^ __float_as_uint(y[k]) ^ __float_as_uint(z[k]);
+        st4(out + 4 * g, w[0], w[1], w[2], w[3]);
+    }
+}
+
+__global__ void __launch_bounds__(256, 3) probe_theta(const float* in, unsigned long long* out, int64_t groups,
+                                                      Params Pin) {
+    PROBE_PROLOGUE
+    (void)tt; (void)tp;
+    for (int64_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
+        float x[4], y[4], z[4];
+        ld12(in, g, x, y, z);
+        int nt[4];
+        bool slow[4];
+        theta2<true>(x, y, P, nt, slow);
+        theta2<true>(x + 2, y + 2, P, nt + 2, slow + 2);
+        unsigned long long w[4];
+        for (int k = 0; k < 4; ++k) w[k] = (unsigned long long)nt[k] ^ __float_as_uint(z[k]) ^ slow[k];
+        st4(out + 4 * g, w[0], w[1], w[2], w[3]);
+    }
+}
+
+__global__ void __launch_bounds__(256, 3) probe_phi(const float* in, unsigned long long* out, int64_t groups,
+                                                    Params Pin) {
+    PROBE_PROLOGUE
+    (void)tt; (void)tp;
+    for (int64_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
+        float x[4], y[4], z[4];
+        ld12(in, g, x, y, z);
+        int nph[4];
+        bool slow[4] = {false, false, false, false};
+        phi2<true>(x, y, z, P, nph, slow);
+        phi2<true>(x + 2, y + 2, z + 2, P, nph + 2, slow + 2);
+        unsigned long long w[4];
+        for (int k = 0; k < 4; ++k) w[k] = (unsigned long long)nph[k] ^ slow[k];
+        st4(out + 4 * g, w[0], w[1], w[2], w[3]);
+    }
+}
+
+__global__ void __launch_bounds__(256, 3) probe_mag(const float* in, unsigned long long* out, int64_t groups,
+                                                    Params Pin) {
+    PROBE_PROLOGUE
+    (void)tt; (void)tp;
+    for (int64_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
+        float x[4], y[4], z[4];
+        ld12(in, g, x, y, z);
+        unsigned long long w[4];
+        for (int k = 0; k < 4; ++k) {
+            bool slow = false;
+            w[k] = (unsigned long long)mag_field_fast(x[k], y[k], z[k], P, slow) ^ slow;
+        }
+        st4(out + 4 * g, w[0], w[1], w[2], w[3]);
     }
 }
 
