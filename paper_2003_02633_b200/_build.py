@@ -52,7 +52,7 @@ def _compile_cmd(src: Path, obj: Path, verbose: bool) -> list[str]:
 COMMON_DEPS = ["vc3_device.cuh", "vc3_rt.h"]
 EXTRA_DEPS = {"vc3_fused_as.cu": ["vc3_fused.cuh", "vc3_kern_common.cuh"],
               "vc3_fused.cu": ["vc3_kern_common.cuh"],
-              "vc3_kernels.cu": ["vc3_kern_common.cuh"]}
+              "vc3_kernels.cu": ["vc3_kern_common.cuh", "vc3_fused.cuh"]}
 
 
 def _defines_stamp(obj_dir: Path) -> Path:

@@ -86,14 +86,23 @@ __global__ void __launch_bounds__(kThreads, MINB)
     // are free
     int64_t g = gtid();
     u64x4 un = {0, 0, 0, 0}, vn = un;
-    if (PREFETCH && g < groups) {
+    if ((PREFETCH == 1 || PREFETCH == 2) && g < groups) {
         un = ld_stream_u4(a + 4 * g);
         vn = ld_stream_u4(b + 4 * g);
     }
     for (; g < groups; g += gstride()) {
         u64x4 u, v;
         const int64_t gn = g + gstride();
-        if (PREFETCH) {
+        if (PREFETCH >= 3) {
+            // 3 / 4: the words of the step one / two grid strides ahead are
+            // prefetched into L2, so this thread's next loads hit L2
+            const int64_t gp = g + (PREFETCH - 2) * gstride();
+            if (gp < groups) {
+                prefetch_l2(a + 4 * gp);
+                prefetch_l2(b + 4 * gp);
+            }
+        }
+        if (PREFETCH == 1 || PREFETCH == 2) {
             u = un;
             v = vn;
             if (PREFETCH == 1 && gn < groups) {
@@ -360,8 +369,11 @@ __global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
 // step through two compress_as2 pairs; the range exceptions take the generic
 // compress_one (warp-uniform branch).  Non-finite inputs are counted (the
 // host raises NonFiniteInput; their words are unspecified, as in vc3_compress).
-template <class LAY>
-__global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS)
+#ifndef VC3_COMPRESS_PF
+#define VC3_COMPRESS_PF 0
+#endif
+template <class LAY, int MINB = VC3_FUSED_MIN_BLOCKS, int PF = VC3_COMPRESS_PF>
+__global__ void __launch_bounds__(kThreads, MINB)
     k_compress_as(const float* __restrict__ xyz, unsigned long long* __restrict__ out, int64_t n,
                   Params Pin, bool vec, int32_t* __restrict__ nonfinite) {
     Params P = Pin;
@@ -369,6 +381,13 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS)
     int bad = 0;
     const int64_t groups = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
+        if (PF) {  // L2 prefetch of the 48 bytes PF grid strides ahead
+            const int64_t gp = g + PF * gstride();
+            if (gp < groups) {
+                prefetch_l2(xyz + 12 * gp);
+                prefetch_l2(xyz + 12 * gp + 8);
+            }
+        }
         const float4 A = ld_stream_f4(xyz + 12 * g), B = ld_stream_f4(xyz + 12 * g + 4),
                      C = ld_stream_f4(xyz + 12 * g + 8);
         const float x[4] = {A.x, A.w, B.z, C.y}, y[4] = {A.y, B.x, B.w, C.z}, z[4] = {A.z, B.y, C.x, C.w};
@@ -425,6 +444,8 @@ int launch_add(const unsigned long long* a, const unsigned long long* b, unsigne
             case 4: fn = exact ? k_add_as<true, DefaultLayout, 4, 2> : k_add_as<false, DefaultLayout, 4, 2>; break;
             case 5: fn = exact ? k_add_as<true, DefaultLayout, 2, 2> : k_add_as<false, DefaultLayout, 2, 2>; break;
             case 3: fn = exact ? k_add_as2<true, DefaultLayout, 4> : k_add_as2<false, DefaultLayout, 4>; break;
+            case 10: fn = exact ? k_add_as<true, DefaultLayout, 3, 3> : k_add_as<false, DefaultLayout, 3, 3>; break;
+            case 11: fn = exact ? k_add_as<true, DefaultLayout, 3, 4> : k_add_as<false, DefaultLayout, 3, 4>; break;
             default: fn = exact ? k_add_as<true, DefaultLayout> : k_add_as<false, DefaultLayout>;
         }
     } else {
@@ -478,7 +499,20 @@ int launch_compress(const float* xyz, unsigned long long* w, int64_t n, const Pa
     int64_t blocks = (items + kThreads - 1) / kThreads;
     const int64_t cap = (int64_t)sm_count() * VC3_COMPRESS_CTAS_PER_SM;
     blocks = blocks > cap ? cap : (blocks < 1 ? 1 : blocks);
-    if (def)
+    int v = 0;
+#ifdef VC3_TUNE
+    static const int tune = getenv("VC3_TUNE_C") ? atoi(getenv("VC3_TUNE_C")) : 0;
+    v = tune;
+#endif
+    if (def && v == 1)
+        k_compress_as<DefaultLayout, 3><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);
+    else if (def && v == 2)
+        k_compress_as<DefaultLayout, 4, 1><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);
+    else if (def && v == 3)
+        k_compress_as<DefaultLayout, 3, 1><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);
+    else if (def && v == 4)
+        k_compress_as<DefaultLayout, 4, 2><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);
+    else if (def)
         k_compress_as<DefaultLayout><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);
     else
         k_compress_as<RuntimeLayout><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);

@@ -27,6 +27,9 @@ constexpr int kThreads = 256;
 #ifndef VC3_RK_CELL
 #define VC3_RK_CELL 0
 #endif
+#ifndef VC3_DECOMP_FUSED
+#define VC3_DECOMP_FUSED 0  // 1: decompress with the fused path's decode (A/B)
+#endif
 #ifndef VC3_DECOMP_STAGE
 #define VC3_DECOMP_STAGE 1
 #endif
@@ -84,6 +87,10 @@ __device__ __forceinline__ float4 ld_stream_f4(const float* p) {
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                  : "l"(p));
     return v;
+}
+// L2 prefetch of a line a later grid-stride step reads (no registers held)
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 // sm_100 256-bit global accesses (LDG/STG .256): four words per instruction
 struct u64x4 {
