@@ -5,7 +5,6 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
-#include <cstdlib>
 #include <type_traits>
 
 #include "../../include/vc3_b200.h"
@@ -26,12 +25,12 @@ constexpr unsigned kAllSingle = 7u;
 // the compress range exceptions (the generic bit-exact compress_one).
 template <bool EXACT>
 __device__ __forceinline__ void decode4(const unsigned long long w[4], const Params& P,
-                                        const double2* tt, const double2* tp, const double2* full,
-                                        double tol2, float x[4], float y[4], float z[4]) {
+                                        const DecTab& T, const double2* full, double tol2,
+                                        float x[4], float y[4], float z[4]) {
     unsigned redo = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-        redo |= (unsigned)decode_fused<EXACT>(w[k], P, tt, tp, tol2, x[k], y[k], z[k]) << k;
+        redo |= (unsigned)decode_fused<EXACT>(w[k], P, T, tol2, x[k], y[k], z[k]) << k;
     if (EXACT && __any_sync(__activemask(), redo != 0u)) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -67,133 +66,24 @@ constexpr bool kBounded = std::is_same<LAY, DefaultLayout>::value;
 #ifndef VC3_ADD_AS_MIN_BLOCKS
 #define VC3_ADD_AS_MIN_BLOCKS 3  // measured: 3 resident CTAs (80 registers, no spills) beat 4 (64, spills)
 #endif
-template <bool EXACT, class LAY, int MINB = VC3_ADD_AS_MIN_BLOCKS, int PREFETCH = 0>
-__global__ void __launch_bounds__(kThreads, MINB)
+template <bool EXACT, class LAY>
+__global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
     k_add_as(const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
              unsigned long long* __restrict__ c, int64_t n, Params Pin, bool vec,
              const double2* __restrict__ gtab, const double2* __restrict__ full) {
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
-    load_table<true>(s_tab, gtab, P);
-    const double2* tt = s_tab;
-    const double2* tp = s_tab + P.p_base;
+    load_table_fused(s_tab, gtab, P);
+    const DecTab T = dec_tab(s_tab, P);
     const double tol2 = EXACT ? exact_tol<true>(full, P) : 0.0;
     const int64_t groups = vec ? n / 4 : 0;
-    // PREFETCH 1: the next step's words are loaded before this step's decode
-    // (register double buffering); 2: loaded after the decodes, so their
-    // latency hides behind the compress half while the decode's registers
-    // are free
-    int64_t g = gtid();
-    u64x4 un = {0, 0, 0, 0}, vn = un;
-    if ((PREFETCH == 1 || PREFETCH == 2) && g < groups) {
-        un = ld_stream_u4(a + 4 * g);
-        vn = ld_stream_u4(b + 4 * g);
-    }
-    for (; g < groups; g += gstride()) {
-        u64x4 u, v;
-        const int64_t gn = g + gstride();
-        if (PREFETCH >= 3) {
-            // 3 / 4: the words of the step one / two grid strides ahead are
-            // prefetched into L2, so this thread's next loads hit L2
-            const int64_t gp = g + (PREFETCH - 2) * gstride();
-            if (gp < groups) {
-                prefetch_l2(a + 4 * gp);
-                prefetch_l2(b + 4 * gp);
-            }
-        }
-        if (PREFETCH == 1 || PREFETCH == 2) {
-            u = un;
-            v = vn;
-            if (PREFETCH == 1 && gn < groups) {
-                un = ld_stream_u4(a + 4 * gn);
-                vn = ld_stream_u4(b + 4 * gn);
-            }
-        } else {
-            u = ld_stream_u4(a + 4 * g);
-            v = ld_stream_u4(b + 4 * g);
-        }
+    for (int64_t g = gtid(); g < groups; g += gstride()) {
+        const u64x4 u = ld_stream_u4(a + 4 * g), v = ld_stream_u4(b + 4 * g);
         const unsigned long long wa[4] = {u.x, u.y, u.z, u.w}, wb[4] = {v.x, v.y, v.z, v.w};
         float xa[4], ya[4], za[4], xb[4], yb[4], zb[4], x[4], y[4], z[4];
-        decode4<EXACT>(wa, P, tt, tp, full, tol2, xa, ya, za);
-        decode4<EXACT>(wb, P, tt, tp, full, tol2, xb, yb, zb);
-#pragma unroll
-        for (int k = 0; k < 4; k += 2) {
-            add_pairs(xa + k, xb + k, x + k);
-            add_pairs(ya + k, yb + k, y + k);
-            add_pairs(za + k, zb + k, z + k);
-        }
-        if (PREFETCH == 2 && gn < groups) {
-            un = ld_stream_u4(a + 4 * gn);
-            vn = ld_stream_u4(b + 4 * gn);
-        }
-        unsigned long long w[4];
-        encode4<kBounded<LAY>>(x, y, z, P, w);
-        st_u4(c + 4 * g, w[0], w[1], w[2], w[3]);
-    }
-    for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
-        float x1, y1, z1, x2, y2, z2;
-        const unsigned long long wa = a[i], wb = b[i];
-        if (decode_fused<EXACT>(wa, P, tt, tp, tol2, x1, y1, z1)) decode_redo(wa, P, full, x1, y1, z1);
-        if (decode_fused<EXACT>(wb, P, tt, tp, tol2, x2, y2, z2)) decode_redo(wb, P, full, x2, y2, z2);
-        c[i] = compress_one<kAllSingle, true, true>(__fadd_rn(x1, x2), __fadd_rn(y1, y2),
-                                                    __fadd_rn(z1, z2), P);
-    }
-}
-
-// Words staged through shared memory by cp.async (LDGSTS), two stages: the
-// next step's 64 bytes per thread are in flight while this step computes,
-// with no registers held for them.  Stage layout chunk-major (16-byte chunk k
-// of thread t at (k * T + t) * 16) so the copies and the LDS.128 reads are
-// bank-conflict free.
-__device__ __forceinline__ void cp_async16(uint32_t smem, const void* g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
-
-template <bool EXACT, class LAY, int T, int MINB>
-__global__ void __launch_bounds__(T, MINB)
-    k_add_as_cp(const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
-                unsigned long long* __restrict__ c, int64_t n, Params Pin, bool vec,
-                const double2* __restrict__ gtab, const double2* __restrict__ full) {
-    Params P = Pin;
-    LAY::apply(P);
-    extern __shared__ double2 s_tab[];
-    load_table<true>(s_tab, gtab, P);
-    const double2* tt = s_tab;
-    const double2* tp = s_tab + P.p_base;
-    const double tol2 = EXACT ? exact_tol<true>(full, P) : 0.0;
-    const int64_t groups = vec ? n / 4 : 0;
-    const uint4* stage = reinterpret_cast<const uint4*>(s_tab + P.tab_n);
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(stage) + threadIdx.x * 16u;
-    auto issue = [&](int64_t gi, int st) {
-        const uint32_t s0 = sbase + (uint32_t)(st * 4 * T * 16);
-        const unsigned long long* pa = a + 4 * gi;
-        const unsigned long long* pb = b + 4 * gi;
-        if (gi < groups) {
-            cp_async16(s0, pa);
-            cp_async16(s0 + T * 16, pa + 2);
-            cp_async16(s0 + 2 * T * 16, pb);
-            cp_async16(s0 + 3 * T * 16, pb + 2);
-        }
-        cp_async_commit();  // (an empty group at the end keeps wait_group 1 uniform)
-    };
-    int64_t g = gtid();
-    issue(g, 0);
-    int st = 0;
-    for (; g < groups; g += gstride(), st ^= 1) {
-        issue(g + gstride(), st ^ 1);
-        cp_async_wait1();  // this step's group (own slots only: no barrier needed)
-        const uint4* q = stage + st * 4 * T + threadIdx.x;
-        const uint4 q0 = q[0], q1 = q[T], q2 = q[2 * T], q3 = q[3 * T];
-        const unsigned long long wa[4] = {((unsigned long long)q0.y << 32) | q0.x, ((unsigned long long)q0.w << 32) | q0.z,
-                                          ((unsigned long long)q1.y << 32) | q1.x, ((unsigned long long)q1.w << 32) | q1.z};
-        const unsigned long long wb[4] = {((unsigned long long)q2.y << 32) | q2.x, ((unsigned long long)q2.w << 32) | q2.z,
-                                          ((unsigned long long)q3.y << 32) | q3.x, ((unsigned long long)q3.w << 32) | q3.z};
-        float xa[4], ya[4], za[4], xb[4], yb[4], zb[4], x[4], y[4], z[4];
-        decode4<EXACT>(wa, P, tt, tp, full, tol2, xa, ya, za);
-        decode4<EXACT>(wb, P, tt, tp, full, tol2, xb, yb, zb);
+        decode4<EXACT>(wa, P, T, full, tol2, xa, ya, za);
+        decode4<EXACT>(wb, P, T, full, tol2, xb, yb, zb);
 #pragma unroll
         for (int k = 0; k < 4; k += 2) {
             add_pairs(xa + k, xb + k, x + k);
@@ -204,55 +94,11 @@ __global__ void __launch_bounds__(T, MINB)
         encode4<kBounded<LAY>>(x, y, z, P, w);
         st_u4(c + 4 * g, w[0], w[1], w[2], w[3]);
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float x1, y1, z1, x2, y2, z2;
         const unsigned long long wa = a[i], wb = b[i];
-        if (decode_fused<EXACT>(wa, P, tt, tp, tol2, x1, y1, z1)) decode_redo(wa, P, full, x1, y1, z1);
-        if (decode_fused<EXACT>(wb, P, tt, tp, tol2, x2, y2, z2)) decode_redo(wb, P, full, x2, y2, z2);
-        c[i] = compress_one<kAllSingle, true, true>(__fadd_rn(x1, x2), __fadd_rn(y1, y2),
-                                                    __fadd_rn(z1, z2), P);
-    }
-}
-
-// Two vectors per thread step (one compress pair): half the live state of
-// k_add_as, 16-byte word accesses.
-template <bool EXACT, class LAY, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
-    k_add_as2(const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
-              unsigned long long* __restrict__ c, int64_t n, Params Pin, bool vec,
-              const double2* __restrict__ gtab, const double2* __restrict__ full) {
-    Params P = Pin;
-    LAY::apply(P);
-    extern __shared__ double2 s_tab[];
-    load_table<true>(s_tab, gtab, P);
-    const double2* tt = s_tab;
-    const double2* tp = s_tab + P.p_base;
-    const double tol2 = EXACT ? exact_tol<true>(full, P) : 0.0;
-    const int64_t pairs = vec ? n / 2 : 0;
-    for (int64_t g = gtid(); g < pairs; g += gstride()) {
-        const ulonglong2 u = ld_stream_u2(a + 2 * g), v = ld_stream_u2(b + 2 * g);
-        const unsigned long long w4[4] = {u.x, u.y, v.x, v.y};
-        float xs[4], ys[4], zs[4], x[2], y[2], z[2];
-        decode4<EXACT>(w4, P, tt, tp, full, tol2, xs, ys, zs);
-        add_pairs(xs, xs + 2, x);
-        add_pairs(ys, ys + 2, y);
-        add_pairs(zs, zs + 2, z);
-        unsigned long long w[2];
-        bool slow[2];
-        compress_as2(x, y, z, P, w, slow);
-        if (__any_sync(__activemask(), slow[0] | slow[1])) {
-#pragma unroll
-            for (int k = 0; k < 2; ++k)
-                if (slow[k]) w[k] = compress_one<kAllSingle, true, true>(x[k], y[k], z[k], P);
-        }
-        st_u2(c + 2 * g, w[0], w[1]);
-    }
-    for (int64_t i = pairs * 2 + gtid(); i < n; i += gstride()) {
-        float x1, y1, z1, x2, y2, z2;
-        const unsigned long long wa = a[i], wb = b[i];
-        if (decode_fused<EXACT>(wa, P, tt, tp, tol2, x1, y1, z1)) decode_redo(wa, P, full, x1, y1, z1);
-        if (decode_fused<EXACT>(wb, P, tt, tp, tol2, x2, y2, z2)) decode_redo(wb, P, full, x2, y2, z2);
+        if (decode_fused<EXACT>(wa, P, T, tol2, x1, y1, z1)) decode_redo(wa, P, full, x1, y1, z1);
+        if (decode_fused<EXACT>(wb, P, T, tol2, x2, y2, z2)) decode_redo(wb, P, full, x2, y2, z2);
         c[i] = compress_one<kAllSingle, true, true>(__fadd_rn(x1, x2), __fadd_rn(y1, y2),
                                                     __fadd_rn(z1, z2), P);
     }
@@ -269,9 +115,8 @@ __global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
-    load_table<true>(s_tab, gtab, P);
-    const double2* tt = s_tab;
-    const double2* tp = s_tab + P.p_base;
+    load_table_fused(s_tab, gtab, P);
+    const DecTab T = dec_tab(s_tab, P);
     const double tol2 = EXACT ? exact_tol<true>(full, P) : 0.0;
     const int64_t groups = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
@@ -282,8 +127,8 @@ __global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
                      : "l"(yw + 4 * g));
         const unsigned long long wa[4] = {u.x, u.y, u.z, u.w}, wb[4] = {v.x, v.y, v.z, v.w};
         float xa[4], ya[4], za[4], xb[4], yb[4], zb[4], x[4], y[4], z[4];
-        decode4<EXACT>(wa, P, tt, tp, full, tol2, xa, ya, za);
-        decode4<EXACT>(wb, P, tt, tp, full, tol2, xb, yb, zb);
+        decode4<EXACT>(wa, P, T, full, tol2, xa, ya, za);
+        decode4<EXACT>(wb, P, T, full, tol2, xb, yb, zb);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             x[k] = __fadd_rn(__fmul_rn(al, xa[k]), xb[k]);
@@ -297,8 +142,8 @@ __global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float x1, y1, z1, x2, y2, z2;
         const unsigned long long wa = xw[i], wb = yw[i];
-        if (decode_fused<EXACT>(wa, P, tt, tp, tol2, x1, y1, z1)) decode_redo(wa, P, full, x1, y1, z1);
-        if (decode_fused<EXACT>(wb, P, tt, tp, tol2, x2, y2, z2)) decode_redo(wb, P, full, x2, y2, z2);
+        if (decode_fused<EXACT>(wa, P, T, tol2, x1, y1, z1)) decode_redo(wa, P, full, x1, y1, z1);
+        if (decode_fused<EXACT>(wb, P, T, tol2, x2, y2, z2)) decode_redo(wb, P, full, x2, y2, z2);
         yo[i] = compress_one<kAllSingle, true, true>(__fadd_rn(__fmul_rn(al, x1), x2),
                                                      __fadd_rn(__fmul_rn(al, y1), y2),
                                                      __fadd_rn(__fmul_rn(al, z1), z2), P);
@@ -321,9 +166,8 @@ __global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
-    load_table<true>(s_tab, gtab, P);
-    const double2* tt = s_tab;
-    const double2* tp = s_tab + P.p_base;
+    load_table_fused(s_tab, gtab, P);
+    const DecTab T = dec_tab(s_tab, P);
     const double tol2 = EXACT ? exact_tol<true>(full, P) : 0.0;
     const int64_t groups = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
@@ -336,9 +180,9 @@ __global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
         const unsigned long long wq[4] = {uq.x, uq.y, uq.z, uq.w}, wd[4] = {ud.x, ud.y, ud.z, ud.w},
                                  wr[4] = {ur.x, ur.y, ur.z, ur.w};
         float qx[4], qy[4], qz[4], dx[4], dy[4], dz[4], rx[4], ry[4], rz[4];
-        decode4<EXACT>(wq, P, tt, tp, full, tol2, qx, qy, qz);
-        decode4<EXACT>(wd, P, tt, tp, full, tol2, dx, dy, dz);
-        decode4<EXACT>(wr, P, tt, tp, full, tol2, rx, ry, rz);
+        decode4<EXACT>(wq, P, T, full, tol2, qx, qy, qz);
+        decode4<EXACT>(wd, P, T, full, tol2, dx, dy, dz);
+        decode4<EXACT>(wr, P, T, full, tol2, rx, ry, rz);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             rk_math<EXACT>(ca, cb, dt, qx[k], dx[k], rx[k]);
@@ -354,9 +198,9 @@ __global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float q0, q1, q2, d0, d1, d2, r0, r1, r2;
         const unsigned long long wq = q[i], wd = dq[i], wr = R[i];
-        if (decode_fused<EXACT>(wq, P, tt, tp, tol2, q0, q1, q2)) decode_redo(wq, P, full, q0, q1, q2);
-        if (decode_fused<EXACT>(wd, P, tt, tp, tol2, d0, d1, d2)) decode_redo(wd, P, full, d0, d1, d2);
-        if (decode_fused<EXACT>(wr, P, tt, tp, tol2, r0, r1, r2)) decode_redo(wr, P, full, r0, r1, r2);
+        if (decode_fused<EXACT>(wq, P, T, tol2, q0, q1, q2)) decode_redo(wq, P, full, q0, q1, q2);
+        if (decode_fused<EXACT>(wd, P, T, tol2, d0, d1, d2)) decode_redo(wd, P, full, d0, d1, d2);
+        if (decode_fused<EXACT>(wr, P, T, tol2, r0, r1, r2)) decode_redo(wr, P, full, r0, r1, r2);
         rk_math<EXACT>(ca, cb, dt, q0, d0, r0);
         rk_math<EXACT>(ca, cb, dt, q1, d1, r1);
         rk_math<EXACT>(ca, cb, dt, q2, d2, r2);
@@ -369,11 +213,8 @@ __global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
 // step through two compress_as2 pairs; the range exceptions take the generic
 // compress_one (warp-uniform branch).  Non-finite inputs are counted (the
 // host raises NonFiniteInput; their words are unspecified, as in vc3_compress).
-#ifndef VC3_COMPRESS_PF
-#define VC3_COMPRESS_PF 0
-#endif
-template <class LAY, int MINB = VC3_FUSED_MIN_BLOCKS, int PF = VC3_COMPRESS_PF>
-__global__ void __launch_bounds__(kThreads, MINB)
+template <class LAY>
+__global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS)
     k_compress_as(const float* __restrict__ xyz, unsigned long long* __restrict__ out, int64_t n,
                   Params Pin, bool vec, int32_t* __restrict__ nonfinite) {
     Params P = Pin;
@@ -381,13 +222,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
     int bad = 0;
     const int64_t groups = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
-        if (PF) {  // L2 prefetch of the 48 bytes PF grid strides ahead
-            const int64_t gp = g + PF * gstride();
-            if (gp < groups) {
-                prefetch_l2(xyz + 12 * gp);
-                prefetch_l2(xyz + 12 * gp + 8);
-            }
-        }
         const float4 A = ld_stream_f4(xyz + 12 * g), B = ld_stream_f4(xyz + 12 * g + 4),
                      C = ld_stream_f4(xyz + 12 * g + 8);
         const float x[4] = {A.x, A.w, B.z, C.y}, y[4] = {A.y, B.x, B.w, C.z}, z[4] = {A.z, B.y, C.x, C.w};
@@ -409,64 +243,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
 
 namespace vc3 {
 namespace as {
-// Launch the all-single fused add (table layouts).  Returns a vc3_status.
-int launch_add(const unsigned long long* a, const unsigned long long* b, unsigned long long* c,
-               int64_t n, const Params& P, bool def, bool exact, bool vec, const double2* tab,
-               const double2* full, cudaStream_t s) {
-    using Fn = void (*)(const unsigned long long*, const unsigned long long*, unsigned long long*,
-                        int64_t, Params, bool, const double2*, const double2*);
-    Fn fn;
-    int threads = kThreads, per_sm = VC3_ADD_CTAS_PER_SM;
-    size_t smem = table_smem(P);
-    int v = 0;
-#ifdef VC3_TUNE
-    static const int tune = getenv("VC3_TUNE") ? atoi(getenv("VC3_TUNE")) : 0;
-    v = tune;
-#endif
-    if (def && v == 7) {
-        fn = exact ? k_add_as_cp<true, DefaultLayout, 512, 2> : k_add_as_cp<false, DefaultLayout, 512, 2>;
-        threads = 512;
-        per_sm = 2;
-        smem += 2 * 4 * 512 * 16;
-    } else if (def && v == 8) {
-        fn = exact ? k_add_as_cp<true, DefaultLayout, 256, 3> : k_add_as_cp<false, DefaultLayout, 256, 3>;
-        per_sm = 3;
-        smem += 2 * 4 * 256 * 16;
-    } else if (def && v == 9) {
-        fn = exact ? k_add_as_cp<true, DefaultLayout, 512, 2> : k_add_as_cp<false, DefaultLayout, 512, 2>;
-        threads = 512;
-        per_sm = 24;
-        smem += 2 * 4 * 512 * 16;
-    } else if (def) {
-        switch (v) {
-            case 1: fn = exact ? k_add_as<true, DefaultLayout, 3> : k_add_as<false, DefaultLayout, 3>; break;
-            case 2: fn = exact ? k_add_as<true, DefaultLayout, 3, 2> : k_add_as<false, DefaultLayout, 3, 2>; break;
-            case 4: fn = exact ? k_add_as<true, DefaultLayout, 4, 2> : k_add_as<false, DefaultLayout, 4, 2>; break;
-            case 5: fn = exact ? k_add_as<true, DefaultLayout, 2, 2> : k_add_as<false, DefaultLayout, 2, 2>; break;
-            case 3: fn = exact ? k_add_as2<true, DefaultLayout, 4> : k_add_as2<false, DefaultLayout, 4>; break;
-            case 10: fn = exact ? k_add_as<true, DefaultLayout, 3, 3> : k_add_as<false, DefaultLayout, 3, 3>; break;
-            case 11: fn = exact ? k_add_as<true, DefaultLayout, 3, 4> : k_add_as<false, DefaultLayout, 3, 4>; break;
-            default: fn = exact ? k_add_as<true, DefaultLayout> : k_add_as<false, DefaultLayout>;
-        }
-    } else {
-        fn = exact ? k_add_as<true, RuntimeLayout> : k_add_as<false, RuntimeLayout>;
-    }
-    if (const int st = ensure_smem((const void*)fn, smem)) return st;
-#ifdef VC3_TUNE
-    static const int tune_grid = getenv("VC3_TUNE_GRID") ? atoi(getenv("VC3_TUNE_GRID")) : 0;
-    if (tune_grid) per_sm = tune_grid;
-#endif
-    const int64_t items = vec ? (n + 3) / 4 : n;
-    int64_t blocks = (items + threads - 1) / threads;
-    const int64_t cap = (int64_t)sm_count() * per_sm;
-    blocks = blocks > cap ? cap : (blocks < 1 ? 1 : blocks);
-    fn<<<(unsigned)blocks, threads, smem, s>>>(a, b, c, n, P, vec, tab, full);
-    return launch_status();
-}
+
+// Shared memory of the fused kernels: the table with replicated residual
+// sections (load_table_fused).
+size_t fused_smem(const Params& P) { return (size_t)P.tabf_n * sizeof(double2); }
 
 template <typename KFn, typename... Args>
 int launch_table_kernel(KFn fn, const Params& P, int64_t n, bool vec, cudaStream_t s, Args... args) {
-    const size_t smem = table_smem(P);
+    const size_t smem = fused_smem(P);
     if (const int st = ensure_smem((const void*)fn, smem)) return st;
     const int64_t items = vec ? (n + 3) / 4 : n;
     int64_t blocks = (items + kThreads - 1) / kThreads;
@@ -474,6 +258,15 @@ int launch_table_kernel(KFn fn, const Params& P, int64_t n, bool vec, cudaStream
     blocks = blocks > cap ? cap : (blocks < 1 ? 1 : blocks);
     fn<<<(unsigned)blocks, kThreads, smem, s>>>(args...);
     return launch_status();
+}
+
+// Launch the all-single fused add (table layouts).  Returns a vc3_status.
+int launch_add(const unsigned long long* a, const unsigned long long* b, unsigned long long* c,
+               int64_t n, const Params& P, bool def, bool exact, bool vec, const double2* tab,
+               const double2* full, cudaStream_t s) {
+    auto fn = def ? (exact ? k_add_as<true, DefaultLayout> : k_add_as<false, DefaultLayout>)
+                  : (exact ? k_add_as<true, RuntimeLayout> : k_add_as<false, RuntimeLayout>);
+    return launch_table_kernel(fn, P, n, vec, s, a, b, c, n, P, vec, tab, full);
 }
 
 int launch_axpy(float al, const unsigned long long* x, const unsigned long long* y,
@@ -499,20 +292,7 @@ int launch_compress(const float* xyz, unsigned long long* w, int64_t n, const Pa
     int64_t blocks = (items + kThreads - 1) / kThreads;
     const int64_t cap = (int64_t)sm_count() * VC3_COMPRESS_CTAS_PER_SM;
     blocks = blocks > cap ? cap : (blocks < 1 ? 1 : blocks);
-    int v = 0;
-#ifdef VC3_TUNE
-    static const int tune = getenv("VC3_TUNE_C") ? atoi(getenv("VC3_TUNE_C")) : 0;
-    v = tune;
-#endif
-    if (def && v == 1)
-        k_compress_as<DefaultLayout, 3><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);
-    else if (def && v == 2)
-        k_compress_as<DefaultLayout, 4, 1><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);
-    else if (def && v == 3)
-        k_compress_as<DefaultLayout, 3, 1><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);
-    else if (def && v == 4)
-        k_compress_as<DefaultLayout, 4, 2><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);
-    else if (def)
+    if (def)
         k_compress_as<DefaultLayout><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);
     else
         k_compress_as<RuntimeLayout><<<(unsigned)blocks, kThreads, 0, s>>>(xyz, w, n, P, vec, nonfinite);

@@ -27,9 +27,6 @@ constexpr int kThreads = 256;
 #ifndef VC3_RK_CELL
 #define VC3_RK_CELL 0
 #endif
-#ifndef VC3_DECOMP_FUSED
-#define VC3_DECOMP_FUSED 0  // 1: decompress with the fused path's decode (A/B)
-#endif
 #ifndef VC3_DECOMP_STAGE
 #define VC3_DECOMP_STAGE 1
 #endif
@@ -88,10 +85,6 @@ __device__ __forceinline__ float4 ld_stream_f4(const float* p) {
                  : "l"(p));
     return v;
 }
-// L2 prefetch of a line a later grid-stride step reads (no registers held)
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
 // sm_100 256-bit global accesses (LDG/STG .256): four words per instruction
 struct u64x4 {
     unsigned long long x, y, z, w;
@@ -144,6 +137,19 @@ __device__ __forceinline__ void load_table(double2* sm, const double2* __restric
         for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = g[i];
         __syncthreads();
     }
+}
+
+// The fused kernels' copy (Params::tabf_n entries): the table up to the
+// residual sections as is, then each residual entry replicated 2^rep times.
+__device__ __forceinline__ void load_table_fused(double2* sm, const double2* __restrict__ g,
+                                                 const Params& P) {
+    for (int i = threadIdx.x; i < P.tabf_n; i += blockDim.x) {
+        const int src = i < P.rt_base    ? i
+                        : i < P.rpf_base ? P.rt_base + ((i - P.rt_base) >> P.rt_rep)
+                                         : P.rp_base + ((i - P.rpf_base) >> P.rp_rep);
+        sm[i] = g[src];
+    }
+    __syncthreads();
 }
 
 // ----- dispatch helpers ----------------------------------------------------------

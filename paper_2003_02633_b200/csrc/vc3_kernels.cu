@@ -339,8 +339,12 @@ int ensure_smem(const void* func, size_t bytes) {
     std::lock_guard<std::mutex> lock(mu);
     auto it = done.find(key);
     if (it != done.end() && it->second >= bytes) return VC3_OK;
-    const int st = cuda_status(
+    int st = cuda_status(
         cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    // all of the unified L1 as shared memory: several table copies per SM
+    // (the streams bypass L1: ld.global.nc.L1::no_allocate)
+    if (st == VC3_OK)
+        st = cuda_status(cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     if (st == VC3_OK) done[key] = bytes;
     return st;
 }
@@ -438,31 +442,6 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
         const int64_t gn = g + gstride();
         if (gn < groups) wn = ld_stream_u4(w + 4 * gn);
         float o[12];
-#if VC3_DECOMP_FUSED
-        if (TABLE) {
-            // the fused path's decode (bump-indexed table, 32-bit magnitude;
-            // exact mode: two-level residual, redo under a warp vote), then
-            // the reference's explicit (+0, +0, +0) for a zero field
-            const unsigned long long w4[4] = {u.x, u.y, u.z, u.w};
-            unsigned redo = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                redo |= (unsigned)decode_fused<EXACT>(w4[k], P, tt, tp, 2.0 * tol, o[3 * k], o[3 * k + 1],
-                                                      o[3 * k + 2]) << k;
-            if (EXACT && __any_sync(__activemask(), redo != 0u)) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if ((redo >> k) & 1u) decode_redo(w4[k], P, full, o[3 * k], o[3 * k + 1], o[3 * k + 2]);
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const bool zero = (w4[k] >> (P.p + P.t)) == 0ull;
-                o[3 * k] = zero ? 0.0f : o[3 * k];
-                o[3 * k + 1] = zero ? 0.0f : o[3 * k + 1];
-                o[3 * k + 2] = zero ? 0.0f : o[3 * k + 2];
-            }
-        } else
-#endif
         {
             decompress_one<TABLE, false, EXACT>(u.x, P, tt, tp, o[0], o[1], o[2], full, tol);
             decompress_one<TABLE, false, EXACT>(u.y, P, tt, tp, o[3], o[4], o[5], full, tol);

@@ -30,8 +30,7 @@ __device__ __forceinline__ void st4(unsigned long long* p, unsigned long long a,
     Params P = Pin;                                    \
     Lay::apply(P);                                     \
     extern __shared__ double2 s_tab[];                 \
-    const double2* tt = s_tab;                         \
-    const double2* tp = s_tab + P.p_base;              \
+    const DecTab T = dec_tab(s_tab, P);                \
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
 
 // stage: two decodes of the fused add (contract / exact), sums stored as floats
@@ -47,8 +46,8 @@ __global__ void __launch_bounds__(256, 4) probe_decode2(const unsigned long long
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             float x1, y1, z1, x2, y2, z2;
-            if (decode_fused<EXACT>(wa[k], P, tt, tp, tol2, x1, y1, z1)) x1 = -x1;
-            if (decode_fused<EXACT>(wb[k], P, tt, tp, tol2, x2, y2, z2)) x2 = -x2;
+            if (decode_fused<EXACT>(wa[k], P, T, tol2, x1, y1, z1)) x1 = -x1;
+            if (decode_fused<EXACT>(wb[k], P, T, tol2, x2, y2, z2)) x2 = -x2;
             o[3 * k] = __fadd_rn(x1, x2);
             o[3 * k + 1] = __fadd_rn(y1, y2);
             o[3 * k + 2] = __fadd_rn(z1, z2);
@@ -64,8 +63,7 @@ __global__ void __launch_bounds__(256, 4) probe_decode2(const unsigned long long
 __global__ void __launch_bounds__(256, 4) probe_compress(const float* in, unsigned long long* out,
                                                          int64_t groups, Params Pin) {
     PROBE_PROLOGUE
-    (void)tt;
-    (void)tp;
+    (void)T;
     for (int64_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
         const float4* s = reinterpret_cast<const float4*>(in + 12 * g);
         const float4 A = s[0], B = s[1], C = s[2];
@@ -85,8 +83,7 @@ __global__ void __launch_bounds__(256, 4) probe_compress(const float* in, unsign
 __global__ void __launch_bounds__(256, 4) probe_compress_r1(const float* in, unsigned long long* out,
                                                             int64_t groups, Params Pin) {
     PROBE_PROLOGUE
-    (void)tt;
-    (void)tp;
+    (void)T;
     for (int64_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
         const float4* s = reinterpret_cast<const float4*>(in + 12 * g);
         const float4 A = s[0], B = s[1], C = s[2];
@@ -109,8 +106,8 @@ __global__ void __launch_bounds__(256, 4) probe_add(const unsigned long long* a,
         unsigned redo = 0;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            redo |= (unsigned)decode_fused<EXACT>(wa[k], P, tt, tp, tol2, xa[k], ya[k], za[k]) << k;
-            redo |= (unsigned)decode_fused<EXACT>(wb[k], P, tt, tp, tol2, xb[k], yb[k], zb[k]) << (k + 4);
+            redo |= (unsigned)decode_fused<EXACT>(wa[k], P, T, tol2, xa[k], ya[k], za[k]) << k;
+            redo |= (unsigned)decode_fused<EXACT>(wb[k], P, T, tol2, xb[k], yb[k], zb[k]) << (k + 4);
         }
         if (EXACT && __any_sync(__activemask(), redo != 0u)) xa[0] = -xa[0];
 #pragma unroll
@@ -153,7 +150,7 @@ __global__ void __launch_bounds__(256, 3) probe_copy(const float* in, unsigned l
 __global__ void __launch_bounds__(256, 3) probe_theta(const float* in, unsigned long long* out, int64_t groups,
                                                       Params Pin) {
     PROBE_PROLOGUE
-    (void)tt; (void)tp;
+    (void)T;
     for (int64_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
         float x[4], y[4], z[4];
         ld12(in, g, x, y, z);
@@ -170,7 +167,7 @@ __global__ void __launch_bounds__(256, 3) probe_theta(const float* in, unsigned 
 __global__ void __launch_bounds__(256, 3) probe_phi(const float* in, unsigned long long* out, int64_t groups,
                                                     Params Pin) {
     PROBE_PROLOGUE
-    (void)tt; (void)tp;
+    (void)T;
     for (int64_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
         float x[4], y[4], z[4];
         ld12(in, g, x, y, z);
@@ -187,7 +184,7 @@ __global__ void __launch_bounds__(256, 3) probe_phi(const float* in, unsigned lo
 __global__ void __launch_bounds__(256, 3) probe_mag(const float* in, unsigned long long* out, int64_t groups,
                                                     Params Pin) {
     PROBE_PROLOGUE
-    (void)tt; (void)tp;
+    (void)T;
     for (int64_t g = blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
         float x[4], y[4], z[4];
         ld12(in, g, x, y, z);
