@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "../../include/vc3_b200.h"
@@ -254,7 +255,12 @@ int launch_table_kernel(KFn fn, const Params& P, int64_t n, bool vec, cudaStream
     if (const int st = ensure_smem((const void*)fn, smem)) return st;
     const int64_t items = vec ? (n + 3) / 4 : n;
     int64_t blocks = (items + kThreads - 1) / kThreads;
-    const int64_t cap = (int64_t)sm_count() * VC3_ADD_CTAS_PER_SM;
+    int per_sm = VC3_AS_CTAS_PER_SM;
+#ifdef VC3_TUNE
+    static const int tune_grid = getenv("VC3_TUNE_GRID") ? atoi(getenv("VC3_TUNE_GRID")) : 0;
+    if (tune_grid > 0) per_sm = tune_grid;
+#endif
+    const int64_t cap = (int64_t)sm_count() * per_sm;
     blocks = blocks > cap ? cap : (blocks < 1 ? 1 : blocks);
     fn<<<(unsigned)blocks, kThreads, smem, s>>>(args...);
     return launch_status();

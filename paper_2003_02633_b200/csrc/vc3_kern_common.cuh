@@ -32,8 +32,16 @@ constexpr int kThreads = 256;
 #endif
 // grid caps in CTAs per SM for the streaming kernels (grid-stride beyond);
 // more CTAs than resident slots balance the tail across SMs (measured)
+#ifndef VC3_DECOMP_CELL
+#define VC3_DECOMP_CELL 0  // decompress's boundary test: 0 two-conversion, 1 cell test (vc3_device.cuh)
+#endif
 #ifndef VC3_ADD_CTAS_PER_SM
 #define VC3_ADD_CTAS_PER_SM 48
+#endif
+// grid cap of the all-single table kernels (3 resident per SM; 12 per SM
+// measured 120.5 vs 118.8 Gvec/s contract, 105.6 vs 105.4 exact at 48)
+#ifndef VC3_AS_CTAS_PER_SM
+#define VC3_AS_CTAS_PER_SM 12
 #endif
 #ifndef VC3_COMPRESS_CTAS_PER_SM
 #define VC3_COMPRESS_CTAS_PER_SM 48

@@ -422,7 +422,10 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
-    const double tol = EXACT ? exact_tol(full, P) : 0.0;
+    // the boundary test and its tolerance form must agree: the cell test
+    // takes the doubled tolerance (exact_tol<true>), the two-conversion test
+    // the plain one
+    const double tol = EXACT ? exact_tol<VC3_DECOMP_CELL != 0>(full, P) : 0.0;
     const int64_t groups = vec ? n / 4 : 0;
 #if VC3_DECOMP_STAGE
     // per-warp shared staging of the array-of-structs output: each lane's 48 B
@@ -443,10 +446,10 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
         if (gn < groups) wn = ld_stream_u4(w + 4 * gn);
         float o[12];
         {
-            decompress_one<TABLE, false, EXACT>(u.x, P, tt, tp, o[0], o[1], o[2], full, tol);
-            decompress_one<TABLE, false, EXACT>(u.y, P, tt, tp, o[3], o[4], o[5], full, tol);
-            decompress_one<TABLE, false, EXACT>(u.z, P, tt, tp, o[6], o[7], o[8], full, tol);
-            decompress_one<TABLE, false, EXACT>(u.w, P, tt, tp, o[9], o[10], o[11], full, tol);
+            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.x, P, tt, tp, o[0], o[1], o[2], full, tol);
+            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.y, P, tt, tp, o[3], o[4], o[5], full, tol);
+            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.z, P, tt, tp, o[6], o[7], o[8], full, tol);
+            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.w, P, tt, tp, o[9], o[10], o[11], full, tol);
         }
 #if VC3_DECOMP_STAGE
         stage[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
@@ -476,7 +479,7 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float x, y, z;
-        decompress_one<TABLE, false, EXACT>(w[i], P, tt, tp, x, y, z, full, tol);
+        decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(w[i], P, tt, tp, x, y, z, full, tol);
         xyz[3 * i] = x;
         xyz[3 * i + 1] = y;
         xyz[3 * i + 2] = z;
