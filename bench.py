@@ -365,11 +365,14 @@ def run_secondary(args, vc3b, lib, dev, stream, n):
     del mom
     k = [0]
 
-    def rk():
+    def rk(flags=0):
         s_ = k[0] % 5
         k[0] += 1
-        lib.vc3_rk_stage(float(fields.LSRK_A[s_]), float(fields.LSRK_B[s_]), 1e-3, q.data_ptr(),
-                         dq.data_ptr(), R.data_ptr(), npts, cl, pol.mask, stream.cuda_stream)
+        lib.vc3_rk_stage_ex(float(fields.LSRK_A[s_]), float(fields.LSRK_B[s_]), 1e-3, q.data_ptr(),
+                            dq.data_ptr(), R.data_ptr(), npts, cl, pol.mask, flags, stream.cuda_stream)
+
+    def rk_contract():
+        rk(1)
 
     def rk32():
         s_ = k[0] % 5
@@ -381,12 +384,15 @@ def run_secondary(args, vc3b, lib, dev, stream, n):
     rk(); rk32()
     torch.cuda.synchronize()
     tc = time_region(rk, steps, stream, torch)
+    rk_contract()
+    tcc = time_region(rk_contract, steps, stream, torch)
     tf = time_region(rk32, steps, stream, torch)
     out["C4_rk_stage_icv"] = {
         "n_points": npts, "field": "ICV beta=5 gamma=1.4 psi=30deg, k=4 FR points, "
                                    "[n_upts][n_elem] rows", "unit": UNIT,
         "compressed_gvec_s": npts / (tc * 1e-3) / 1e9,
         "compressed_hbm_gb_s": 40 * npts / (tc * 1e-3) / 1e9,
+        "compressed_contract_gvec_s": npts / (tcc * 1e-3) / 1e9,
         "fp32_gvec_s": npts / (tf * 1e-3) / 1e9,
         "fp32_hbm_gb_s": 60 * npts / (tf * 1e-3) / 1e9,
         "speedup_vs_fp32": tf / tc}
