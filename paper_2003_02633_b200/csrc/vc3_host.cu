@@ -56,11 +56,8 @@ constexpr int kMaxIo = 3;  // host operands + result per call
 // byte instead of 2) and do not evict the cache.  The trailing sfence makes
 // the stores globally visible before the slice is reported done (the DMA or
 // the caller reads them next).
-#ifndef VC3_HOST_NT
-#define VC3_HOST_NT 1
-#endif
 void copy_stream(void* dst, const void* src, size_t n) {
-#if defined(__x86_64__) && VC3_HOST_NT
+#if defined(__x86_64__)
     char* d = (char*)dst;
     const char* s = (const char*)src;
     const size_t head = std::min(n, (size_t)((16 - ((uintptr_t)d & 15)) & 15));
@@ -83,6 +80,13 @@ void copy_stream(void* dst, const void* src, size_t n) {
 #endif
 }
 
+// Copies into the pinned ring: streaming stores (1) or plain stores (0: the
+// ring's lines can stay in the last-level cache, where the copy engine's
+// reads find them when the slots are small)
+#ifndef VC3_HOST_NT_IN
+#define VC3_HOST_NT_IN 1
+#endif
+
 // A small pool of host threads for the staging copies (memcpy into / out of
 // the pinned ring): one memcpy thread reaches ~10 GB/s, PCIe 5 ~55 GB/s.
 class CopyPool {
@@ -95,7 +99,7 @@ class CopyPool {
         return *pool;
     }
     // copy `bytes` in `nthreads_` slices; returns when all slices are done
-    void copy(void* dst, const void* src, size_t bytes) {
+    void copy(void* dst, const void* src, size_t bytes, bool nt) {
         const int parts = (int)std::max<size_t>(1, std::min<size_t>(workers_.size() + 1, bytes >> 20));
         const size_t step = (bytes + parts - 1) / parts;
         {
@@ -104,12 +108,20 @@ class CopyPool {
                 const size_t lo = std::min(bytes, step * i), hi = std::min(bytes, lo + step);
                 if (hi > lo) {
                     ++pending_;
-                    tasks_.push_back([=] { copy_stream((char*)dst + lo, (const char*)src + lo, hi - lo); });
+                    tasks_.push_back([=] {
+                        if (nt)
+                            copy_stream((char*)dst + lo, (const char*)src + lo, hi - lo);
+                        else
+                            std::memcpy((char*)dst + lo, (const char*)src + lo, hi - lo);
+                    });
                 }
             }
         }
         cv_.notify_all();
-        copy_stream(dst, src, std::min(bytes, step));  // this thread's slice
+        if (nt)  // this thread's slice
+            copy_stream(dst, src, std::min(bytes, step));
+        else
+            std::memcpy(dst, src, std::min(bytes, step));
         std::unique_lock<std::mutex> lock(mu_);
         done_cv_.wait(lock, [&] { return pending_ == 0; });
     }
@@ -260,7 +272,7 @@ int pipeline(const void* const (&in)[NIN], const int (&in_bytes)[NIN], void* out
         const int b = (int)(kk % nbuf);
         const int64_t off = kk * chunk, cnt = std::min(chunk, n - off);
         if (cudaStreamSynchronize(ctx->streams[b]) != cudaSuccess) return VC3_ERR_CUDA;
-        pool.copy((char*)out + off * out_bytes, ctx->stage[b][NIN], cnt * out_bytes);
+        pool.copy((char*)out + off * out_bytes, ctx->stage[b][NIN], cnt * out_bytes, true);
         return VC3_OK;
     };
     for (int64_t k = 0; k < nchunks && !st; ++k) {
@@ -272,7 +284,7 @@ int pipeline(const void* const (&in)[NIN], const int (&in_bytes)[NIN], void* out
         for (int i = 0; i < NIN; ++i) {
             const char* src = (const char*)in[i] + off * in_bytes[i];
             if (staged) {
-                pool.copy(ctx->stage[b][i], src, cnt * in_bytes[i]);
+                pool.copy(ctx->stage[b][i], src, cnt * in_bytes[i], VC3_HOST_NT_IN != 0);
                 src = ctx->stage[b][i];
             }
             if (cudaMemcpyAsync(dev_in[b][i], src, cnt * in_bytes[i], cudaMemcpyHostToDevice, s) !=

@@ -32,9 +32,6 @@ constexpr int kThreads = 256;
 #endif
 // grid caps in CTAs per SM for the streaming kernels (grid-stride beyond);
 // more CTAs than resident slots balance the tail across SMs (measured)
-#ifndef VC3_DECOMP_FUSED
-#define VC3_DECOMP_FUSED 0  // 1: decompress with the fused kernels' decode (A/B)
-#endif
 #ifndef VC3_DECOMP_CELL
 #define VC3_DECOMP_CELL 0  // decompress's boundary test: 0 two-conversion, 1 cell test (vc3_device.cuh)
 #endif

@@ -410,7 +410,9 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_compress(con
 // EXACT: bit-identical to the reference's libm decode (boundary components
 // redone from its own tables); !EXACT: the fast table decode, each component
 // the reference's float32 or one ulp from it.
-template <bool TABLE, class LAY, bool EXACT = true>
+// STAGE: the per-warp shared staging of the output (measured: contract mode
+// 264 staged vs 243 direct, exact mode 248 staged vs 262 direct Gword/s).
+template <bool TABLE, class LAY, bool EXACT = true, bool STAGE = VC3_DECOMP_STAGE != 0>
 __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_decompress(const unsigned long long* __restrict__ w,
                                                          float* __restrict__ xyz, int64_t n,
                                                          Params Pin, bool vec,
@@ -419,28 +421,20 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
-    // FUSED: the fused kernels' decode (vc3_fused.cuh decode_fused: replicated
-    // two-level table, exact test with warp-vote redo)
-    constexpr bool FUSED = TABLE && VC3_DECOMP_FUSED;
-    if (FUSED)
-        load_table_fused(s_tab, gtab, P);
-    else
-        load_table<TABLE>(s_tab, gtab, P);
+    load_table<TABLE>(s_tab, gtab, P);
     const double2* tt = s_tab;
     const double2* tp = s_tab + P.p_base;
-    const DecTab TB = dec_tab(s_tab, P);
     // the boundary test and its tolerance form must agree: the cell test
     // takes the doubled tolerance (exact_tol<true>), the two-conversion test
     // the plain one
-    const double tol = EXACT ? exact_tol<FUSED || VC3_DECOMP_CELL != 0>(full, P) : 0.0;
+    const double tol = EXACT ? exact_tol<VC3_DECOMP_CELL != 0>(full, P) : 0.0;
     const int64_t groups = vec ? n / 4 : 0;
-#if VC3_DECOMP_STAGE
     // per-warp shared staging of the array-of-structs output: each lane's 48 B
     // go to shared memory, then the warp writes 3 x 512 contiguous bytes
-    float4* stage = reinterpret_cast<float4*>(s_tab + (TABLE ? (FUSED ? P.tabf_n : P.tab_n) : 0)) +
-                    (threadIdx.x >> 5) * 96;
+    float4* stage = !STAGE ? nullptr : reinterpret_cast<float4*>(s_tab + (TABLE ? P.tab_n : 0)) + (threadIdx.x >> 5) * 96;
     const int lane = threadIdx.x & 31;
-#endif
+    (void)stage;
+    (void)lane;
     // register double buffering: the next step's words are in flight while
     // this step decodes (one CTA holds only 1024 threads at 49 KB of table)
     int64_t g = gtid();
@@ -453,32 +447,13 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
         const int64_t gn = g + gstride();
         if (gn < groups) wn = ld_stream_u4(w + 4 * gn);
         float o[12];
-        if (FUSED) {
-            const unsigned long long w4[4] = {u.x, u.y, u.z, u.w};
-            unsigned redo = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                redo |= (unsigned)decode_fused<EXACT>(w4[k], P, TB, tol, o[3 * k], o[3 * k + 1], o[3 * k + 2]) << k;
-            if (EXACT && __any_sync(__activemask(), redo != 0u)) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if ((redo >> k) & 1u) decode_redo(w4[k], P, full, o[3 * k], o[3 * k + 1], o[3 * k + 2]);
-            }
-            // a zero field decodes to (+0, +0, +0) (_kernels.py:183-185)
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const bool zero = (w4[k] >> (P.p + P.t)) == 0ull;
-                o[3 * k] = zero ? 0.0f : o[3 * k];
-                o[3 * k + 1] = zero ? 0.0f : o[3 * k + 1];
-                o[3 * k + 2] = zero ? 0.0f : o[3 * k + 2];
-            }
-        } else {
+        {
             decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.x, P, tt, tp, o[0], o[1], o[2], full, tol);
             decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.y, P, tt, tp, o[3], o[4], o[5], full, tol);
             decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.z, P, tt, tp, o[6], o[7], o[8], full, tol);
             decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.w, P, tt, tp, o[9], o[10], o[11], full, tol);
         }
-#if VC3_DECOMP_STAGE
+        if constexpr (STAGE) {
         stage[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
         stage[3 * lane + 1] = make_float4(o[4], o[5], o[6], o[7]);
         stage[3 * lane + 2] = make_float4(o[8], o[9], o[10], o[11]);
@@ -495,14 +470,14 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
             }
         }
         __syncwarp();
-#else
-        if (live) {
+        } else {
+        if (g < groups) {
             float* dst = xyz + 12 * g;
             st_f4(dst, o[0], o[1], o[2], o[3]);
             st_f4(dst + 4, o[4], o[5], o[6], o[7]);
             st_f4(dst + 8, o[8], o[9], o[10], o[11]);
         }
-#endif
+        }
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float x, y, z;
@@ -881,19 +856,20 @@ int vc3_decompress_ex(const uint64_t* words, float* xyz, int64_t n, vc3_layout l
     const int64_t cap = (int64_t)sm_count() * VC3_DECOMP_CTAS_PER_SM;
     const unsigned grid = (unsigned)(blocks > cap ? cap : (blocks < 1 ? 1 : blocks));
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t stage = VC3_DECOMP_STAGE ? (size_t)VC3_DECOMP_THREADS * 48 : 0;  // 1.5 KB per warp
+    // output staging: 1.5 KB per warp (contract mode and wide layouts only)
+    const bool staged = !(P.table_mode && exact);
+    const size_t stage = staged ? (size_t)VC3_DECOMP_THREADS * 48 : 0;
     const bool def = is_default_layout(layout);
     using KFn = void (*)(const unsigned long long*, float*, int64_t, Params, bool, const double2*,
                          const double2*);
     KFn fn;
     if (!P.table_mode)  // wide layouts: the reference-angle polynomial (no table, no exactness test)
-        fn = k_decompress<false, RuntimeLayout>;
+        fn = k_decompress<false, RuntimeLayout, true, true>;
     else if (def)
-        fn = exact ? k_decompress<true, DefaultLayout, true> : k_decompress<true, DefaultLayout, false>;
+        fn = exact ? k_decompress<true, DefaultLayout, true, false> : k_decompress<true, DefaultLayout, false, true>;
     else
-        fn = exact ? k_decompress<true, RuntimeLayout, true> : k_decompress<true, RuntimeLayout, false>;
-    const size_t smem =
-        (P.table_mode ? (VC3_DECOMP_FUSED ? (size_t)P.tabf_n * sizeof(double2) : table_smem(P)) : 0) + stage;
+        fn = exact ? k_decompress<true, RuntimeLayout, true, false> : k_decompress<true, RuntimeLayout, false, true>;
+    const size_t smem = (P.table_mode ? table_smem(P) : 0) + stage;
     st = ensure_smem((const void*)fn, smem);
     if (st) return st;
     fn<<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab, full);
