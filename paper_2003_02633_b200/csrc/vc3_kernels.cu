@@ -11,6 +11,7 @@
 // at the default layout, opt-in shared memory) from global memory into
 // shared memory.
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 #include <cmath>
 #include <cstdint>
