@@ -67,16 +67,25 @@ constexpr bool kBounded = std::is_same<LAY, DefaultLayout>::value;
 #ifndef VC3_ADD_AS_MIN_BLOCKS
 #define VC3_ADD_AS_MIN_BLOCKS 3  // measured: 3 resident CTAs (80 registers, no spills) beat 4 (64, spills)
 #endif
-template <bool EXACT, class LAY>
-__global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
+// CFG: the shared-memory copy and CTA shape (fused_copy): 0 = 3 CTAs x 256
+// threads per SM; 1, 2 = one CTA x 768 threads per SM with replicated grids
+// (theta x2 / phi x4, or theta x4 / phi x4)
+template <int CFG>
+constexpr int kAsThreads = CFG ? 768 : kThreads;
+template <int CFG>
+constexpr int kAsMinBlocks = CFG ? 1 : VC3_ADD_AS_MIN_BLOCKS;
+
+template <bool EXACT, class LAY, int CFG = 0>
+__global__ void __launch_bounds__(kAsThreads<CFG>, kAsMinBlocks<CFG>)
     k_add_as(const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
              unsigned long long* __restrict__ c, int64_t n, Params Pin, bool vec,
              const double2* __restrict__ gtab, const double2* __restrict__ full) {
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
-    load_table_fused(s_tab, gtab, P);
-    const DecTab T = dec_tab(s_tab, P);
+    const FusedCopy F = fused_copy<CFG>(P);
+    load_table_fused(s_tab, gtab, P, F);
+    const DecTab T = dec_tab(s_tab, F);
     const double tol2 = EXACT ? exact_tol<true>(full, P) : 0.0;
     const int64_t groups = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
@@ -108,16 +117,17 @@ __global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
 // K4 axpy, all-single: y' = compress(alpha * decode(x) + decode(y)), the
 // float32 product and sum rounded separately (scalar: a packed product may
 // not feed a packed sum, vc3_fused.cuh).  y may alias y_out.
-template <bool EXACT, class LAY>
-__global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
+template <bool EXACT, class LAY, int CFG = 0>
+__global__ void __launch_bounds__(kAsThreads<CFG>, kAsMinBlocks<CFG>)
     k_axpy_as(float al, const unsigned long long* __restrict__ xw, const unsigned long long* yw,
               unsigned long long* yo, int64_t n, Params Pin, bool vec,
               const double2* __restrict__ gtab, const double2* __restrict__ full) {
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
-    load_table_fused(s_tab, gtab, P);
-    const DecTab T = dec_tab(s_tab, P);
+    const FusedCopy F = fused_copy<CFG>(P);
+    load_table_fused(s_tab, gtab, P, F);
+    const DecTab T = dec_tab(s_tab, F);
     const double tol2 = EXACT ? exact_tol<true>(full, P) : 0.0;
     const int64_t groups = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
@@ -159,16 +169,17 @@ __device__ __forceinline__ void rk_math(float ca, float cb, float dt, float& q, 
     q = __fadd_rn(q, __fmul_rn(cb, d));
 }
 
-template <bool EXACT, class LAY>
-__global__ void __launch_bounds__(kThreads, VC3_ADD_AS_MIN_BLOCKS)
+template <bool EXACT, class LAY, int CFG = 0>
+__global__ void __launch_bounds__(kAsThreads<CFG>, kAsMinBlocks<CFG>)
     k_rk_as(float ca, float cb, float dt, unsigned long long* __restrict__ q,
             unsigned long long* __restrict__ dq, const unsigned long long* __restrict__ R, int64_t n,
             Params Pin, bool vec, const double2* __restrict__ gtab, const double2* __restrict__ full) {
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
-    load_table_fused(s_tab, gtab, P);
-    const DecTab T = dec_tab(s_tab, P);
+    const FusedCopy F = fused_copy<CFG>(P);
+    load_table_fused(s_tab, gtab, P, F);
+    const DecTab T = dec_tab(s_tab, F);
     const double tol2 = EXACT ? exact_tol<true>(full, P) : 0.0;
     const int64_t groups = vec ? n / 4 : 0;
     for (int64_t g = gtid(); g < groups; g += gstride()) {
@@ -245,50 +256,97 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS)
 namespace vc3 {
 namespace as {
 
-// Shared memory of the fused kernels: the table with replicated residual
-// sections (load_table_fused).
-size_t fused_smem(const Params& P) { return (size_t)P.tabf_n * sizeof(double2); }
+// Shared memory of the fused kernels: the table copy (fused_copy<CFG>).
+template <int CFG>
+size_t fused_smem(const Params& P) { return (size_t)fused_copy<CFG>(P).n * sizeof(double2); }
 
-template <typename KFn, typename... Args>
+template <int CFG, typename KFn, typename... Args>
 int launch_table_kernel(KFn fn, const Params& P, int64_t n, bool vec, cudaStream_t s, Args... args) {
-    const size_t smem = fused_smem(P);
+    const size_t smem = fused_smem<CFG>(P);
     if (const int st = ensure_smem((const void*)fn, smem)) return st;
+    const int threads = kAsThreads<CFG>;
     const int64_t items = vec ? (n + 3) / 4 : n;
-    int64_t blocks = (items + kThreads - 1) / kThreads;
-    int per_sm = VC3_AS_CTAS_PER_SM;
+    int64_t blocks = (items + threads - 1) / threads;
+    int per_sm = CFG ? VC3_AS1_CTAS_PER_SM : VC3_AS_CTAS_PER_SM;
 #ifdef VC3_TUNE
     static const int tune_grid = getenv("VC3_TUNE_GRID") ? atoi(getenv("VC3_TUNE_GRID")) : 0;
     if (tune_grid > 0) per_sm = tune_grid;
 #endif
     const int64_t cap = (int64_t)sm_count() * per_sm;
     blocks = blocks > cap ? cap : (blocks < 1 ? 1 : blocks);
-    fn<<<(unsigned)blocks, kThreads, smem, s>>>(args...);
+    fn<<<(unsigned)blocks, threads, smem, s>>>(args...);
     return launch_status();
+}
+
+// Copy configuration per operation and mode (fused_copy; measured on 2^28
+// vectors, Gvec/s exact / contract): add 113.3 / 130.0 with CFG 2, 110.4 /
+// 131.1 with CFG 1, 105.4 / 120.4 with CFG 0 (3 x 256 threads); axpy 108.9 /
+// 126.2 (CFG 1) vs 109.1 / 120.4 (CFG 2); RK 60.2 / 67.8 (CFG 2) vs 58.9 /
+// 64.8 (CFG 1).  CFG 2's copy layout is instantiated for the default layout
+// only; other layouts take CFG 1.
+enum AsOp { kOpAdd, kOpAxpy, kOpRk };
+static int as_cfg(AsOp op, bool exact, bool def) {
+    int c = op == kOpAdd ? (exact ? 2 : 1) : (op == kOpAxpy ? 1 : 2);
+#ifdef VC3_TUNE
+    static const int t = getenv("VC3_TUNE_CFG") ? atoi(getenv("VC3_TUNE_CFG")) : -1;
+    if (t >= 0) c = t;
+#endif
+    return c == 2 && !def ? 1 : c;
 }
 
 // Launch the all-single fused add (table layouts).  Returns a vc3_status.
 int launch_add(const unsigned long long* a, const unsigned long long* b, unsigned long long* c,
                int64_t n, const Params& P, bool def, bool exact, bool vec, const double2* tab,
                const double2* full, cudaStream_t s) {
+    const int cfg = as_cfg(kOpAdd, exact, def);
+    if (cfg == 2) {
+        auto fn = exact ? k_add_as<true, DefaultLayout, 2> : k_add_as<false, DefaultLayout, 2>;
+        return launch_table_kernel<2>(fn, P, n, vec, s, a, b, c, n, P, vec, tab, full);
+    }
+    if (cfg == 1) {
+        auto fn = def ? (exact ? k_add_as<true, DefaultLayout, 1> : k_add_as<false, DefaultLayout, 1>)
+                      : (exact ? k_add_as<true, RuntimeLayout, 1> : k_add_as<false, RuntimeLayout, 1>);
+        return launch_table_kernel<1>(fn, P, n, vec, s, a, b, c, n, P, vec, tab, full);
+    }
     auto fn = def ? (exact ? k_add_as<true, DefaultLayout> : k_add_as<false, DefaultLayout>)
                   : (exact ? k_add_as<true, RuntimeLayout> : k_add_as<false, RuntimeLayout>);
-    return launch_table_kernel(fn, P, n, vec, s, a, b, c, n, P, vec, tab, full);
+    return launch_table_kernel<0>(fn, P, n, vec, s, a, b, c, n, P, vec, tab, full);
 }
 
 int launch_axpy(float al, const unsigned long long* x, const unsigned long long* y,
                 unsigned long long* yo, int64_t n, const Params& P, bool def, bool exact, bool vec,
                 const double2* tab, const double2* full, cudaStream_t s) {
+    const int cfg = as_cfg(kOpAxpy, exact, def);
+    if (cfg == 2) {
+        auto fn = exact ? k_axpy_as<true, DefaultLayout, 2> : k_axpy_as<false, DefaultLayout, 2>;
+        return launch_table_kernel<2>(fn, P, n, vec, s, al, x, y, yo, n, P, vec, tab, full);
+    }
+    if (cfg == 1) {
+        auto fn = def ? (exact ? k_axpy_as<true, DefaultLayout, 1> : k_axpy_as<false, DefaultLayout, 1>)
+                      : (exact ? k_axpy_as<true, RuntimeLayout, 1> : k_axpy_as<false, RuntimeLayout, 1>);
+        return launch_table_kernel<1>(fn, P, n, vec, s, al, x, y, yo, n, P, vec, tab, full);
+    }
     auto fn = def ? (exact ? k_axpy_as<true, DefaultLayout> : k_axpy_as<false, DefaultLayout>)
                   : (exact ? k_axpy_as<true, RuntimeLayout> : k_axpy_as<false, RuntimeLayout>);
-    return launch_table_kernel(fn, P, n, vec, s, al, x, y, yo, n, P, vec, tab, full);
+    return launch_table_kernel<0>(fn, P, n, vec, s, al, x, y, yo, n, P, vec, tab, full);
 }
 
 int launch_rk(float ca, float cb, float dt, unsigned long long* q, unsigned long long* dq,
               const unsigned long long* R, int64_t n, const Params& P, bool def, bool exact,
               bool vec, const double2* tab, const double2* full, cudaStream_t s) {
+    const int cfg = as_cfg(kOpRk, exact, def);
+    if (cfg == 2) {
+        auto fn = exact ? k_rk_as<true, DefaultLayout, 2> : k_rk_as<false, DefaultLayout, 2>;
+        return launch_table_kernel<2>(fn, P, n, vec, s, ca, cb, dt, q, dq, R, n, P, vec, tab, full);
+    }
+    if (cfg == 1) {
+        auto fn = def ? (exact ? k_rk_as<true, DefaultLayout, 1> : k_rk_as<false, DefaultLayout, 1>)
+                      : (exact ? k_rk_as<true, RuntimeLayout, 1> : k_rk_as<false, RuntimeLayout, 1>);
+        return launch_table_kernel<1>(fn, P, n, vec, s, ca, cb, dt, q, dq, R, n, P, vec, tab, full);
+    }
     auto fn = def ? (exact ? k_rk_as<true, DefaultLayout> : k_rk_as<false, DefaultLayout>)
                   : (exact ? k_rk_as<true, RuntimeLayout> : k_rk_as<false, RuntimeLayout>);
-    return launch_table_kernel(fn, P, n, vec, s, ca, cb, dt, q, dq, R, n, P, vec, tab, full);
+    return launch_table_kernel<0>(fn, P, n, vec, s, ca, cb, dt, q, dq, R, n, P, vec, tab, full);
 }
 
 // The all-single compress (layouts with t <= 25, p <= 24: clamp-free buckets).

@@ -43,6 +43,9 @@ constexpr int kThreads = 256;
 #ifndef VC3_AS_CTAS_PER_SM
 #define VC3_AS_CTAS_PER_SM 12
 #endif
+#ifndef VC3_AS1_CTAS_PER_SM
+#define VC3_AS1_CTAS_PER_SM 1  // CFG 1, 2 (one 768-thread CTA per SM: persistent)
+#endif
 #ifndef VC3_COMPRESS_CTAS_PER_SM
 #define VC3_COMPRESS_CTAS_PER_SM 48
 #endif
@@ -147,14 +150,13 @@ __device__ __forceinline__ void load_table(double2* sm, const double2* __restric
     }
 }
 
-// The fused kernels' copy (Params::tabf_n entries): the table up to the
-// residual sections as is, then each residual entry replicated 2^rep times.
-__device__ __forceinline__ void load_table_fused(double2* sm, const double2* __restrict__ g,
-                                                 const Params& P) {
-    for (int i = threadIdx.x; i < P.tabf_n; i += blockDim.x) {
-        const int src = i < P.rt_base    ? i
-                        : i < P.rpf_base ? P.rt_base + ((i - P.rt_base) >> P.rt_rep)
-                                         : P.rp_base + ((i - P.rpf_base) >> P.rp_rep);
+__device__ __forceinline__ void load_table_fused(double2* sm, const double2* __restrict__ g, const Params& P,
+                                                 const FusedCopy& F) {
+    for (int i = threadIdx.x; i < F.n; i += blockDim.x) {
+        const int src = i < F.tp    ? (i >> F.tg)
+                        : i < F.trt ? P.p_base + ((i - F.tp) >> F.pg)
+                        : i < F.trp ? P.rt_base + ((i - F.trt) >> F.rt)
+                                    : P.rp_base + ((i - F.trp) >> F.rp);
         sm[i] = g[src];
     }
     __syncthreads();

@@ -413,8 +413,13 @@ __global__ void __launch_bounds__(kThreads, VC3_FUSED_MIN_BLOCKS) k_compress(con
 // the reference's float32 or one ulp from it.
 // STAGE: the per-warp shared staging of the output (measured: contract mode
 // 264 staged vs 243 direct, exact mode 248 staged vs 262 direct Gword/s).
-template <bool TABLE, class LAY, bool EXACT = true, bool STAGE = VC3_DECOMP_STAGE != 0>
-__global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_decompress(const unsigned long long* __restrict__ w,
+// PREP: log2 replication of the phi grid (lane L reads copy L mod 2^PREP):
+// fewer bank conflicts on its random lookups; MINB: resident CTAs per SM.
+// Contract mode: PREP 2, one CTA per SM (275.5 vs 264.8 Gword/s); exact
+// mode keeps the unreplicated table at 2 CTAs per SM (262 vs 261).
+template <bool TABLE, class LAY, bool EXACT = true, bool STAGE = VC3_DECOMP_STAGE != 0, int PREP_ = 0,
+          int MINB = VC3_DECOMP_MIN_BLOCKS, int TREP_ = 0, int THREADS = VC3_DECOMP_THREADS>
+__global__ void __launch_bounds__(THREADS, MINB) k_decompress(const unsigned long long* __restrict__ w,
                                                          float* __restrict__ xyz, int64_t n,
                                                          Params Pin, bool vec,
                                                          const double2* __restrict__ gtab,
@@ -422,9 +427,18 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     Params P = Pin;
     LAY::apply(P);
     extern __shared__ double2 s_tab[];
-    load_table<TABLE>(s_tab, gtab, P);
-    const double2* tt = s_tab;
-    const double2* tp = s_tab + P.p_base;
+    constexpr int PREP = TABLE ? PREP_ : 0, TREP = TABLE ? TREP_ : 0;
+    const int pb = P.t_n << TREP;  // phi grid start in the (replicated) copy
+    const int tab_n = TABLE ? (PREP || TREP ? pb + (P.p_n << PREP) : P.tab_n) : 0;
+    if (TABLE && (PREP || TREP)) {
+        for (int i = threadIdx.x; i < tab_n; i += blockDim.x)
+            s_tab[i] = gtab[i < pb ? (i >> TREP) : P.p_base + ((i - pb) >> PREP)];
+        __syncthreads();
+    } else {
+        load_table<TABLE>(s_tab, gtab, P);
+    }
+    const double2* tt = s_tab + (TREP ? (threadIdx.x & ((1 << TREP) - 1)) : 0);
+    const double2* tp = s_tab + (PREP || TREP ? pb : P.p_base) + (PREP ? (threadIdx.x & ((1 << PREP) - 1)) : 0);
     // the boundary test and its tolerance form must agree: the cell test
     // takes the doubled tolerance (exact_tol<true>), the two-conversion test
     // the plain one
@@ -432,7 +446,7 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     const int64_t groups = vec ? n / 4 : 0;
     // per-warp shared staging of the array-of-structs output: each lane's 48 B
     // go to shared memory, then the warp writes 3 x 512 contiguous bytes
-    float4* stage = !STAGE ? nullptr : reinterpret_cast<float4*>(s_tab + (TABLE ? P.tab_n : 0)) + (threadIdx.x >> 5) * 96;
+    float4* stage = !STAGE ? nullptr : reinterpret_cast<float4*>(s_tab + tab_n) + (threadIdx.x >> 5) * 96;
     const int lane = threadIdx.x & 31;
     (void)stage;
     (void)lane;
@@ -449,10 +463,10 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
         if (gn < groups) wn = ld_stream_u4(w + 4 * gn);
         float o[12];
         {
-            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.x, P, tt, tp, o[0], o[1], o[2], full, tol);
-            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.y, P, tt, tp, o[3], o[4], o[5], full, tol);
-            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.z, P, tt, tp, o[6], o[7], o[8], full, tol);
-            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(u.w, P, tt, tp, o[9], o[10], o[11], full, tol);
+            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0, PREP, TREP>(u.x, P, tt, tp, o[0], o[1], o[2], full, tol);
+            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0, PREP, TREP>(u.y, P, tt, tp, o[3], o[4], o[5], full, tol);
+            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0, PREP, TREP>(u.z, P, tt, tp, o[6], o[7], o[8], full, tol);
+            decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0, PREP, TREP>(u.w, P, tt, tp, o[9], o[10], o[11], full, tol);
         }
         if constexpr (STAGE) {
         stage[3 * lane] = make_float4(o[0], o[1], o[2], o[3]);
@@ -482,7 +496,7 @@ __global__ void __launch_bounds__(VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS) k_d
     }
     for (int64_t i = groups * 4 + gtid(); i < n; i += gstride()) {
         float x, y, z;
-        decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0>(w[i], P, tt, tp, x, y, z, full, tol);
+        decompress_one<TABLE, false, EXACT, VC3_DECOMP_CELL != 0, PREP, TREP>(w[i], P, tt, tp, x, y, z, full, tol);
         xyz[3 * i] = x;
         xyz[3 * i + 1] = y;
         xyz[3 * i + 2] = z;
@@ -767,6 +781,28 @@ struct RunSpherical {
 }  // namespace
 
 // ===================== extern "C" boundary ====================================
+namespace {
+// One k_decompress configuration: replication of the phi / theta grids
+// (PREP / TREP, log2), CTA size, resident CTAs, grid cap per SM.
+template <bool TABLE, class LAY, bool EXACT, bool STAGE, int PREP, int TREP, int THREADS, int MINB>
+int decomp_launch(const unsigned long long* W, float* xyz, int64_t n, const Params& P, bool vec,
+                  const double2* tab, const double2* full, int per_sm, cudaStream_t s) {
+    auto fn = k_decompress<TABLE, LAY, EXACT, STAGE, PREP, MINB, TREP, THREADS>;
+    const size_t tab_bytes =
+        !TABLE ? 0
+               : (PREP || TREP ? (size_t)((P.t_n << TREP) + (P.p_n << PREP)) * sizeof(double2) : table_smem(P));
+    const size_t smem = tab_bytes + (STAGE ? (size_t)THREADS * 48 : 0);  // staging: 1.5 KB per warp
+    if (const int st = ensure_smem((const void*)fn, smem)) return st;
+    const int64_t items = vec ? (n + 3) / 4 : n;
+    int64_t blocks = (items + THREADS - 1) / THREADS;
+    const int64_t cap = (int64_t)sm_count() * per_sm;
+    blocks = blocks > cap ? cap : (blocks < 1 ? 1 : blocks);
+    fn<<<(unsigned)blocks, THREADS, smem, s>>>(W, xyz, n, P, vec, tab, full);
+    return launch_status();
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* vc3_version(void) { return "vc3-b200 0.2.0 (sm_100a)"; }
@@ -852,29 +888,39 @@ int vc3_decompress_ex(const uint64_t* words, float* xyz, int64_t n, vc3_layout l
     }
     auto W = (const unsigned long long*)words;
     const bool vec = aligned32(words) && aligned16(xyz);
-    const int64_t items = vec ? (n + 3) / 4 : n;
-    int64_t blocks = (items + VC3_DECOMP_THREADS - 1) / VC3_DECOMP_THREADS;
-    const int64_t cap = (int64_t)sm_count() * VC3_DECOMP_CTAS_PER_SM;
-    const unsigned grid = (unsigned)(blocks > cap ? cap : (blocks < 1 ? 1 : blocks));
     cudaStream_t s = (cudaStream_t)stream;
-    // output staging: 1.5 KB per warp (contract mode and wide layouts only)
-    const bool staged = !(P.table_mode && exact);
-    const size_t stage = staged ? (size_t)VC3_DECOMP_THREADS * 48 : 0;
     const bool def = is_default_layout(layout);
-    using KFn = void (*)(const unsigned long long*, float*, int64_t, Params, bool, const double2*,
-                         const double2*);
-    KFn fn;
     if (!P.table_mode)  // wide layouts: the reference-angle polynomial (no table, no exactness test)
-        fn = k_decompress<false, RuntimeLayout, true, true>;
-    else if (def)
-        fn = exact ? k_decompress<true, DefaultLayout, true, false> : k_decompress<true, DefaultLayout, false, true>;
-    else
-        fn = exact ? k_decompress<true, RuntimeLayout, true, false> : k_decompress<true, RuntimeLayout, false, true>;
-    const size_t smem = (P.table_mode ? table_smem(P) : 0) + stage;
-    st = ensure_smem((const void*)fn, smem);
-    if (st) return st;
-    fn<<<grid, VC3_DECOMP_THREADS, smem, s>>>(W, xyz, n, P, vec, tab, full);
-    return launch_status();
+        return decomp_launch<false, RuntimeLayout, true, true, 0, 0, VC3_DECOMP_THREADS, VC3_DECOMP_MIN_BLOCKS>(
+            W, xyz, n, P, vec, tab, full, VC3_DECOMP_CTAS_PER_SM, s);
+    // measured (2^28 words, Gword/s exact / contract): cfg 0 255.3 / 255.6,
+    // cfg 1 259.2 / 275.3, cfg 2 262.2 / 273.0, cfg 3 270.4 / 272.3
+    int cfg = exact ? 3 : 1;
+#ifdef VC3_TUNE
+    static const int tune = getenv("VC3_TUNE_DEC") ? atoi(getenv("VC3_TUNE_DEC")) : -1;
+    if (tune >= 0) cfg = tune;
+#endif
+#define VC3_DEC_GO(LAY)                                                                                   \
+    switch (cfg) {                                                                                        \
+        case 0: /* 2 x 512 threads, unreplicated table */                                                 \
+            return exact ? decomp_launch<true, LAY, true, false, 0, 0, 512, 2>(W, xyz, n, P, vec, tab, full, 4, s) \
+                         : decomp_launch<true, LAY, false, true, 0, 0, 512, 2>(W, xyz, n, P, vec, tab, full, 4, s); \
+        case 1: /* 1 x 512 threads, phi grid x4 */                                                        \
+            return exact ? decomp_launch<true, LAY, true, false, 2, 0, 512, 1>(W, xyz, n, P, vec, tab, full, 2, s) \
+                         : decomp_launch<true, LAY, false, true, 2, 0, 512, 1>(W, xyz, n, P, vec, tab, full, 2, s); \
+        case 2: /* 1 x 768 threads, theta grid x2, phi grid x4 */                                         \
+            return exact ? decomp_launch<true, LAY, true, false, 2, 1, 768, 1>(W, xyz, n, P, vec, tab, full, 1, s) \
+                         : decomp_launch<true, LAY, false, true, 2, 1, 768, 1>(W, xyz, n, P, vec, tab, full, 1, s); \
+        default: /* 1 x 768 threads, theta grid x4, phi grid x2 */                                        \
+            return exact ? decomp_launch<true, LAY, true, false, 1, 2, 768, 1>(W, xyz, n, P, vec, tab, full, 1, s) \
+                         : decomp_launch<true, LAY, false, true, 1, 2, 768, 1>(W, xyz, n, P, vec, tab, full, 1, s); \
+    }
+    if (def) {
+        VC3_DEC_GO(DefaultLayout)
+    } else {
+        VC3_DEC_GO(RuntimeLayout)
+    }
+#undef VC3_DEC_GO
 }
 
 int vc3_decompress(const uint64_t* words, float* xyz, int64_t n, vc3_layout layout, void* stream) {

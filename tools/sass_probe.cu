@@ -30,7 +30,7 @@ __device__ __forceinline__ void st4(unsigned long long* p, unsigned long long a,
     Params P = Pin;                                    \
     Lay::apply(P);                                     \
     extern __shared__ double2 s_tab[];                 \
-    const DecTab T = dec_tab(s_tab, P);                \
+    const DecTab T = dec_tab(s_tab, fused_copy<0>(P)); \
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
 
 // stage: two decodes of the fused add (contract / exact), sums stored as floats
