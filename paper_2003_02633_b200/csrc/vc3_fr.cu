@@ -38,6 +38,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/vc3_b200.h"
 #include "vc3_device.cuh"
@@ -525,6 +526,294 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin) 
     }
 }
 
+// ---- the CTA-pair kernel (tcgen05 cta_group::2) ------------------------------
+// Two CTAs of a cluster share one UMMA M = 256 product per (dimension, split):
+// each holds the A operand of its own 128 elements and half of the operator
+// slice (N / 2 columns), the leader issues the MMA for both, and each CTA's
+// TMEM receives the accumulator rows of its elements.  Per 128 elements the
+// tensor core then reads 4 KB of A and 2 KB of B per MMA instead of 4 + 4, and
+// each CTA copies half of each operator slice: this kernel is bound by
+// shared-memory bandwidth (tensor-core operand reads + decode stores).
+// The peer's stage and accumulator hand-offs reach the leader's barriers
+// through one relay thread (the peer's MMA warp): it waits on the peer's own
+// barrier and arrives on the leader's at cluster scope.
+constexpr int kPairRows = 128;  // elements per CTA; a pair's tile is 256
+
+__host__ __device__ constexpr int pair_half_bytes(int npad) { return npad * kPts * 4 / 2; }
+__host__ __device__ constexpr int pair_stage_bytes(int npad) {
+    return 6 * kASliceBytes + 6 * pair_half_bytes(npad);
+}
+__host__ __device__ constexpr int pa_slice(int lo, int d) { return (lo * 3 + d) * kASliceBytes; }
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_rank(uint64_t* bar, uint32_t rank) {
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+__device__ __forceinline__ void mma2_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"((unsigned short)3)
+        : "memory");
+}
+
+template <bool RAW, class LAY>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsFr, 1) k_fr_div2(FrArgs a, Params Pin) {
+    Params P = Pin;
+    LAY::apply(P);
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int sbytes = pair_stage_bytes(a.npad);
+    const int hb = pair_half_bytes(a.npad);
+    constexpr int esize = RAW ? 12 : 8;
+    constexpr int rbytes = kPts * kPairRows * esize;  // one raw-ring slot
+    unsigned char* stages = smem;
+    unsigned char* rawbuf = smem + (size_t)a.nbuf * sbytes;
+    unsigned char* meta = rawbuf + (size_t)a.nraw * rbytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(meta);
+    uint64_t* empty = full + a.nbuf;
+    uint64_t* acc_full = empty + a.nbuf;  // [2]
+    uint64_t* acc_empty = acc_full + 2;   // [2]
+    uint64_t* raw_full = acc_empty + 2;   // [nraw]
+    uint64_t* raw_empty = raw_full + 8;   // [nraw]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 8);
+    const uint32_t tmem_cols = 2 * a.npad <= 32 ? 32 : 2 * a.npad <= 64 ? 64 : 2 * a.npad <= 128 ? 128
+                             : 2 * a.npad <= 256 ? 256 : 512;
+    const int64_t tiles_per_var = (a.n_elem + 2 * kPairRows - 1) / (2 * kPairRows);
+    const int64_t ntiles = tiles_per_var * a.n_vars;
+    const int64_t pair0 = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < a.nbuf; ++b) {
+            mbar_init(&full[b], kDecodeWarps + 1 + (leader ? 1 : 0));  // + the peer's relay
+            mbar_init(&empty[b], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], kEpiWarps + (leader ? 1 : 0));
+        }
+        for (int r = 0; r < a.nraw; ++r) {
+            mbar_init(&raw_full[r], 1);
+            mbar_init(&raw_empty[r], kDecodeWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < kDecodeWarps) {
+        // ---------------- producers of A (decode): 4 threads per element, 2 points each;
+        // lane pairs hold the two halves of one element's 4-point group, so a
+        // half warp stores one 128-byte core matrix (conflict free)
+        const int row = (threadIdx.x & 255) >> 1, h = 2 * (threadIdx.x >> 8) + (threadIdx.x & 1);  // h in 0..3
+        const int off = canon_off(row, 2 * h);
+        int b = 0, use = 0, r = 0, ruse = 0;
+        for (int64_t t = pair0; t < ntiles; t += npairs) {
+            for (int s = 0; s < a.nst; ++s) {
+                const int nv = min(max(a.ns - (s * kPts + 2 * h), 0), 2);
+                mbar_wait(&raw_full[r], ruse & 1);
+                const unsigned char* rb = rawbuf + (size_t)r * rbytes;
+                float x[2], y[2], z[2];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const unsigned char* e = rb + ((size_t)(2 * h + q) * kPairRows + row) * esize;
+                    if (RAW) {
+                        const float* ef = reinterpret_cast<const float*>(e);
+                        x[q] = q < nv ? ef[0] : 0.f;
+                        y[q] = q < nv ? ef[1] : 0.f;
+                        z[q] = q < nv ? ef[2] : 0.f;
+                    } else {
+                        const unsigned long long wq = q < nv ? *reinterpret_cast<const unsigned long long*>(e) : 0ull;
+                        decode_f32<LAY>(wq, P, x[q], y[q], z[q]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&raw_empty[r]);
+                if (++r == a.nraw) { r = 0; ++ruse; }
+                if (use > 0) mbar_wait(&empty[b], (use - 1) & 1);
+                unsigned char* st = stages + (size_t)b * sbytes;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    const float* v = d == 0 ? x : (d == 1 ? y : z);
+                    float2 hi, lo;
+                    hi.x = tf32_hi(v[0]); lo.x = v[0] - hi.x;
+                    hi.y = tf32_hi(v[1]); lo.y = v[1] - hi.y;
+                    *reinterpret_cast<float2*>(st + pa_slice(0, d) + off) = hi;
+                    *reinterpret_cast<float2*>(st + pa_slice(1, d) + off) = lo;
+                }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&full[b]);
+                if (++b == a.nbuf) { b = 0; ++use; }
+            }
+        }
+    } else if (warp < kDecodeWarps + kEpiWarps) {
+        // ---------------- epilogue: this CTA's 128 elements from its TMEM
+        const int ew = warp - kDecodeWarps;  // == warp % 4: TMEM lane quarter
+        const int64_t cstride = (int64_t)a.n_vars * a.ld;
+        int lt = 0;
+        for (int64_t t = pair0; t < ntiles; t += npairs, ++lt) {
+            const int ab = lt & 1, au = lt >> 1;
+            mbar_wait(&acc_full[ab], au & 1);
+            tc_fence_after();
+            const int c = (int)(t / tiles_per_var);
+            const int64_t ei = (t - (int64_t)c * tiles_per_var) * (2 * kPairRows) + rank * kPairRows + ew * 32 + lane;
+            const bool elive = ei < a.n_elem;
+            float* op = a.out + (int64_t)c * a.ld + ei;
+            const uint32_t tbase = tmem + ((uint32_t)(ew * 32) << 16) + (uint32_t)(ab * a.npad);
+            for (int c0 = 0; c0 < a.npad; c0 += 16) {
+                float v[16];
+                tmem_ld16(tbase + (uint32_t)c0, v);
+                const int kn = min(16, a.ns - c0);
+                if (elive) {
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) {
+                        if (q < kn) op[0] = v[q];
+                        op += cstride;
+                    }
+                } else {
+                    op += 16 * cstride;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[ab]);
+        }
+    } else if (warp == kLoadWarp) {
+        // ---------------- this CTA's half of each operator slice
+        if (lane == 0) {
+            int b = 0, use = 0;
+            for (int64_t t = pair0; t < ntiles; t += npairs) {
+                for (int s = 0; s < a.nst; ++s) {
+                    if (use > 0) mbar_wait(&empty[b], (use - 1) & 1);
+                    unsigned char* dst = stages + (size_t)b * sbytes + 6 * kASliceBytes;
+                    mbar_arrive_tx(&full[b], 6 * hb);
+                    const float* src = a.bprep + (size_t)s * 6 * a.npad * kPts + (size_t)rank * (hb / 4);
+#pragma unroll 1
+                    for (int part = 0; part < 6; ++part)
+                        bulk_g2s(dst + part * hb, src + (size_t)part * a.npad * kPts, hb, &full[b]);
+                    if (++b == a.nbuf) { b = 0; ++use; }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kRawWarp) {
+        // ---------------- flux rows of this CTA's 128 elements
+        if (lane == 0) {
+            const int64_t plane = (int64_t)a.n_vars * a.ld;
+            const unsigned char* src0 = RAW ? reinterpret_cast<const unsigned char*>(a.raw)
+                                            : reinterpret_cast<const unsigned char*>(a.words);
+            int r = 0, ruse = 0;
+            for (int64_t t = pair0; t < ntiles; t += npairs) {
+                const int c = (int)(t / tiles_per_var);
+                const int64_t i0 = (t - (int64_t)c * tiles_per_var) * (2 * kPairRows) + rank * kPairRows;
+                const int64_t left = a.ld - i0;
+                const int64_t cnt = left <= 0 ? 0 : (left < kPairRows ? left : kPairRows);
+                const uint32_t row_bytes = (uint32_t)(cnt * esize);
+                for (int s = 0; s < a.nst; ++s) {
+                    if (ruse > 0) mbar_wait(&raw_empty[r], (ruse - 1) & 1);
+                    const int nrows = min(kPts, a.ns - s * kPts);
+                    unsigned char* dst = rawbuf + (size_t)r * rbytes;
+                    mbar_arrive_tx(&raw_full[r], (uint32_t)nrows * row_bytes);
+                    if (row_bytes)
+                        for (int jj = 0; jj < nrows; ++jj) {
+                            const int64_t j = (int64_t)s * kPts + jj;
+                            bulk_g2s(dst + (size_t)jj * kPairRows * esize,
+                                     src0 + ((j * plane) + (int64_t)c * a.ld + i0) * esize, row_bytes,
+                                     &raw_full[r]);
+                        }
+                    if (++r == a.nraw) { r = 0; ++ruse; }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == kMmaWarp) {
+        if (lane == 0 && leader) {
+            // ---------------- MMA issue for the pair (one thread of the leader)
+            const uint32_t idesc = idesc_tf32(2 * kPairRows, a.npad);
+            const uint64_t desc0 = smem_desc(stages, 128, 256);
+            int b = 0, use = 0, lt = 0;
+            for (int64_t t = pair0; t < ntiles; t += npairs, ++lt) {
+                const int ab = lt & 1, au = lt >> 1;
+                if (au > 0) mbar_wait(&acc_empty[ab], (au - 1) & 1);  // both epilogues drained it
+                tc_fence_after();
+                for (int s = 0; s < a.nst; ++s) {
+                    mbar_wait(&full[b], use & 1);  // both CTAs' stage b
+                    tc_fence_after();
+                    const uint64_t sd = desc0 + (uint64_t)(((uint32_t)b * (uint32_t)sbytes) >> 4);
+                    const uint64_t bd = sd + (uint64_t)((6 * kASliceBytes) >> 4);
+                    const uint32_t acc = tmem + (uint32_t)(ab * a.npad);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        const uint64_t bhi = bd + (uint64_t)((uint32_t)(d * hb) >> 4);
+                        const uint64_t blo = bd + (uint64_t)((uint32_t)((3 + d) * hb) >> 4);
+                        const uint64_t ahi = sd + (uint64_t)(pa_slice(0, d) >> 4);
+                        const uint64_t alo = sd + (uint64_t)(pa_slice(1, d) >> 4);
+                        mma2_tf32(acc, alo, bhi, idesc, (s | d) != 0);
+                        mma2_tf32(acc, ahi, blo, idesc, 1);
+                        mma2_tf32(acc, ahi, bhi, idesc, 1);
+                    }
+                    mma2_commit_both(&empty[b]);
+                    if (++b == a.nbuf) { b = 0; ++use; }
+                }
+                mma2_commit_both(&acc_full[ab]);
+            }
+        } else if (lane == 0) {
+            // ---------------- the peer's relay to the leader's barriers
+            int b = 0, use = 0, lt = 0;
+            for (int64_t t = pair0; t < ntiles; t += npairs, ++lt) {
+                const int ab = lt & 1, au = lt >> 1;
+                if (au > 0) {
+                    mbar_wait(&acc_empty[ab], (au - 1) & 1);
+                    mbar_arrive_rank(&acc_empty[ab], 0);
+                }
+                for (int s = 0; s < a.nst; ++s) {
+                    mbar_wait(&full[b], use & 1);
+                    mbar_arrive_rank(&full[b], 0);
+                    if (++b == a.nbuf) { b = 0; ++use; }
+                }
+            }
+        }
+        __syncwarp();
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
+    }
+}
+
 int npad_for(int ns) { return ((ns + 15) / 16) * 16; }
 int nst_for(int ns) { return (ns + kPts - 1) / kPts; }
 
@@ -550,8 +839,49 @@ int fr_launch(const unsigned long long* words, const float* raw, const float* bp
         if (!layout_ok(*layout)) return VC3_ERR_LAYOUT;
         P = make_params(*layout);
     }
-    const size_t sb = (size_t)stage_bytes(a.npad);
+    // the CTA-pair kernel is opt-in (VC3_FR_PAIR=1 in the environment): it is
+    // correct but measured slower
+    static const bool pair_on = [] {
+        const char* e = getenv("VC3_FR_PAIR");
+        return e && e[0] == '1';
+    }();
     const size_t budget = 227 * 1024 - 1024;
+    {
+        // the CTA-pair kernel (k_fr_div2): bulk flux rows (16-byte aligned
+        // rows), an even grid of clusters
+        const int esize_p = raw ? 12 : 8;
+        const void* src_p = raw ? (const void*)raw : (const void*)words;
+        const bool bulk_p = ((uintptr_t)src_p & 15u) == 0 && (ld % 4) == 0;
+        if (pair_on && bulk_p && sm_count() >= 2) {
+            const size_t sbp = (size_t)pair_stage_bytes(a.npad);
+            const size_t rbp = (size_t)kPts * kPairRows * esize_p;
+            int nbuf = (int)((budget - 2 * rbp) / sbp);
+            if (nbuf > 4) nbuf = 4;
+            if (nbuf > a.nst) nbuf = a.nst;
+            if (nbuf >= 1) {
+                int nraw = (int)((budget - (size_t)nbuf * sbp) / rbp);
+                if (nraw > 8) nraw = 8;
+                a.nbuf = nbuf;
+                a.nraw = nraw;
+                const size_t smem = (size_t)nbuf * sbp + (size_t)nraw * rbp + 1024;
+                const int64_t tiles = ((n_elem + 2 * kPairRows - 1) / (2 * kPairRows)) * n_vars;
+                const int64_t pairs = tiles < sm_count() / 2 ? tiles : sm_count() / 2;
+                const unsigned grid = (unsigned)(2 * pairs);
+#define VC3_FR_GO2(R, L)                                                                 \
+    do {                                                                                 \
+        const int st_ = ensure_smem((const void*)k_fr_div2<R, L>, smem);                \
+        if (st_) return st_;                                                             \
+        k_fr_div2<R, L><<<grid, kThreadsFr, smem, s>>>(a, P);                           \
+    } while (0)
+                if (raw) VC3_FR_GO2(true, RuntimeLayout);
+                else if (is_default_layout(*layout)) VC3_FR_GO2(false, DefaultLayout);
+                else VC3_FR_GO2(false, RuntimeLayout);
+#undef VC3_FR_GO2
+                return launch_status();
+            }
+        }
+    }
+    const size_t sb = (size_t)stage_bytes(a.npad);
     // the raw ring needs 16-byte aligned rows: base pointer, ld multiple of 4
     const int esize = raw ? 12 : 8;
     const void* src = raw ? (const void*)raw : (const void*)words;

@@ -7,6 +7,8 @@ the float32 paths, ragged element counts, padded strides, ns = 8 .. 216.
 Tolerance: 3xTF32 products accumulate in fp32, so each output is checked
 to 2^-18 of sum_j,d |D| |X| (the fp32 sum itself carries ~ns * 2^-24)."""
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
@@ -158,3 +160,44 @@ def test_fr_operator_limits():
     assert lib.vc3_fr_operator_floats(256) > 0
     assert lib.vc3_fr_operator_floats(257) == -1 and lib.vc3_fr_operator_floats(0) == -1
     assert lib.vc3_fr_divergence_f32(None, None, None, 1, 1, 1, 125, None) == -2
+
+
+PAIR_SCRIPT = """
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+from paper_2003_02633_b200 import codec, fr
+out = {{}}
+for k, n_elem, n_vars in ((4, 1000, 5), (1, 37, 2), (2, 300, 3), (5, 260, 1)):
+    ns = (k + 1) ** 3
+    g = torch.Generator(device="cuda").manual_seed(k)
+    F = torch.rand((ns, n_vars, n_elem, 3), device="cuda", generator=g) * 2 - 1
+    words = codec.compress(F.reshape(-1, 3)).reshape(ns, n_vars, n_elem)
+    op = fr.Operator(fr.divergence_operator(k))
+    out[k] = (fr.flux_divergence(words, op).cpu().numpy(), fr.flux_divergence_f32(F, op).cpu().numpy())
+np.savez({path!r}, **{{f"c{{k}}": v[0] for k, v in out.items()}}, **{{f"f{{k}}": v[1] for k, v in out.items()}})
+print("ok")
+"""
+
+
+@pytest.mark.gpu
+def test_fr_pair_kernel_matches(tmp_path):
+    """The opt-in CTA-pair kernel (tcgen05 cta_group::2, VC3_FR_PAIR=1) gives
+    the single-CTA kernel's results to the 3xTF32 accuracy (both paths
+    accumulate the same products in the same order per output)."""
+    import os
+    import subprocess
+    import sys
+
+    root = str(Path(__file__).resolve().parents[1])
+    res = {}
+    for pair in ("0", "1"):
+        path = str(tmp_path / f"fr{pair}.npz")
+        env = dict(os.environ, VC3_FR_PAIR=pair)
+        r = subprocess.run([sys.executable, "-c", PAIR_SCRIPT.format(root=root, path=path)], env=env,
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+        res[pair] = np.load(path)
+    for key in res["0"].files:
+        a, b = res["0"][key], res["1"][key]
+        scale = np.abs(a).max() + 1e-30
+        assert np.abs(a - b).max() <= 2.0 ** -16 * scale, key
