@@ -538,6 +538,7 @@ __global__ void __launch_bounds__(kThreadsFr, 1) k_fr_div(FrArgs a, Params Pin) 
 // through one relay thread (the peer's MMA warp): it waits on the peer's own
 // barrier and arrives on the leader's at cluster scope.
 constexpr int kPairRows = 128;  // elements per CTA; a pair's tile is 256
+constexpr int kPairDecodeWarps = 8;  // 2 threads per element, 4 points each
 
 __host__ __device__ constexpr int pair_half_bytes(int npad) { return npad * kPts * 4 / 2; }
 __host__ __device__ constexpr int pair_stage_bytes(int npad) {
@@ -605,7 +606,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsFr, 1) k_fr_
 
     if (threadIdx.x == 0) {
         for (int b = 0; b < a.nbuf; ++b) {
-            mbar_init(&full[b], kDecodeWarps + 1 + (leader ? 1 : 0));  // + the peer's relay
+            mbar_init(&full[b], kPairDecodeWarps + 1 + (leader ? 1 : 0));  // + the peer's relay
             mbar_init(&empty[b], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -614,7 +615,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsFr, 1) k_fr_
         }
         for (int r = 0; r < a.nraw; ++r) {
             mbar_init(&raw_full[r], 1);
-            mbar_init(&raw_empty[r], kDecodeWarps);
+            mbar_init(&raw_empty[r], kPairDecodeWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -630,22 +631,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsFr, 1) k_fr_
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp < kDecodeWarps) {
-        // ---------------- producers of A (decode): 4 threads per element, 2 points each;
-        // lane pairs hold the two halves of one element's 4-point group, so a
-        // half warp stores one 128-byte core matrix (conflict free)
-        const int row = (threadIdx.x & 255) >> 1, h = 2 * (threadIdx.x >> 8) + (threadIdx.x & 1);  // h in 0..3
-        const int off = canon_off(row, 2 * h);
+    if (warp < kPairDecodeWarps) {
+        // ---------------- producers of A (decode): 2 threads per element, 4 points each
+        // (warps kPairDecodeWarps..kDecodeWarps-1 of the shared CTA shape idle)
+        const int row = threadIdx.x & (kPairRows - 1), h = threadIdx.x / kPairRows;  // h in 0..1
+        const int off = canon_off(row, 4 * h);
         int b = 0, use = 0, r = 0, ruse = 0;
         for (int64_t t = pair0; t < ntiles; t += npairs) {
             for (int s = 0; s < a.nst; ++s) {
-                const int nv = min(max(a.ns - (s * kPts + 2 * h), 0), 2);
+                const int nv = min(max(a.ns - (s * kPts + 4 * h), 0), 4);
                 mbar_wait(&raw_full[r], ruse & 1);
                 const unsigned char* rb = rawbuf + (size_t)r * rbytes;
-                float x[2], y[2], z[2];
+                float x[4], y[4], z[4];
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const unsigned char* e = rb + ((size_t)(2 * h + q) * kPairRows + row) * esize;
+                for (int q = 0; q < 4; ++q) {
+                    const unsigned char* e = rb + ((size_t)(4 * h + q) * kPairRows + row) * esize;
                     if (RAW) {
                         const float* ef = reinterpret_cast<const float*>(e);
                         x[q] = q < nv ? ef[0] : 0.f;
@@ -664,11 +664,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsFr, 1) k_fr_
 #pragma unroll
                 for (int d = 0; d < 3; ++d) {
                     const float* v = d == 0 ? x : (d == 1 ? y : z);
-                    float2 hi, lo;
+                    float4 hi, lo;
                     hi.x = tf32_hi(v[0]); lo.x = v[0] - hi.x;
                     hi.y = tf32_hi(v[1]); lo.y = v[1] - hi.y;
-                    *reinterpret_cast<float2*>(st + pa_slice(0, d) + off) = hi;
-                    *reinterpret_cast<float2*>(st + pa_slice(1, d) + off) = lo;
+                    hi.z = tf32_hi(v[2]); lo.z = v[2] - hi.z;
+                    hi.w = tf32_hi(v[3]); lo.w = v[3] - hi.w;
+                    *reinterpret_cast<float4*>(st + pa_slice(0, d) + off) = hi;
+                    *reinterpret_cast<float4*>(st + pa_slice(1, d) + off) = lo;
                 }
                 fence_async_smem();
                 __syncwarp();
@@ -676,6 +678,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreadsFr, 1) k_fr_
                 if (++b == a.nbuf) { b = 0; ++use; }
             }
         }
+    } else if (warp < kDecodeWarps) {
+        // idle
     } else if (warp < kDecodeWarps + kEpiWarps) {
         // ---------------- epilogue: this CTA's 128 elements from its TMEM
         const int ew = warp - kDecodeWarps;  // == warp % 4: TMEM lane quarter
