@@ -45,12 +45,13 @@ __device__ __forceinline__ long long clip_ll(long long v, long long hi) {
 }
 
 // Compander.encode (analysis.py:364-378)
+template <int KIND>
 __device__ __forceinline__ long long compand_encode(double psi, long long n_max, const VParams& V) {
     const double nm = (double)n_max;
     double raw;
-    if (V.kind == VC3_VARIANT_COSINE) {
+    if (KIND == VC3_VARIANT_COSINE) {
         raw = __ddiv_rn(__dmul_rn(nm, __dsub_rn(1.0, cos(__dmul_rn(kPi, psi)))), 2.0);
-    } else if (V.kind == VC3_VARIANT_TANH) {
+    } else if (KIND == VC3_VARIANT_TANH) {
         const double t = tanh(__dmul_rn(V.gamma, __dsub_rn(__dmul_rn(2.0, psi), 1.0)));
         raw = __dmul_rn(__dmul_rn(V.m, nm), __dadd_rn(t, V.c));
     } else {
@@ -60,13 +61,14 @@ __device__ __forceinline__ long long compand_encode(double psi, long long n_max,
 }
 
 // Compander.decode (analysis.py:380-393)
+template <int KIND>
 __device__ __forceinline__ double compand_decode(long long n, long long n_max, const VParams& V) {
     const double nd = (double)n, nm = (double)n_max;
-    if (V.kind == VC3_VARIANT_COSINE) {
+    if (KIND == VC3_VARIANT_COSINE) {
         const double arg = fmin(fmax(__dsub_rn(1.0, __ddiv_rn(__dmul_rn(2.0, nd), nm)), -1.0), 1.0);
         return __ddiv_rn(acos(arg), kPi);
     }
-    if (V.kind == VC3_VARIANT_TANH) {
+    if (KIND == VC3_VARIANT_TANH) {
         const double u = fmin(fmax(__dsub_rn(__ddiv_rn(nd, __dmul_rn(V.m, nm)), V.c), -V.c), V.c);
         const double psi = __ddiv_rn(__dadd_rn(__ddiv_rn(atanh(u), V.gamma), 1.0), 2.0);
         return fmin(fmax(psi, 0.0), 1.0);
@@ -92,6 +94,8 @@ __device__ __forceinline__ float decode_field(unsigned long long field, const VP
     return __uint_as_float(((unsigned)e8 << 23) | (mant << (23 - V.mb)));
 }
 
+// KIND: the variant, a template parameter so each kernel carries one code path
+template <int KIND>
 __global__ void __launch_bounds__(kThreads) k_compress_variant(const float* __restrict__ xyz,
                                                                unsigned long long* __restrict__ out,
                                                                int64_t n, VParams V,
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(kThreads) k_compress_variant(const float* __re
         }
         long long nt, nph;
         unsigned long long angles;
-        if (V.kind == VC3_VARIANT_SPLIT) {
+        if (KIND == VC3_VARIANT_SPLIT) {
             // _quantize_free (analysis.py:300-306), then joint_encode (:284-291)
             const double ntm = (double)V.nt_max, npm = (double)V.np_max;
             const double vt = __dadd_rn(__ddiv_rn(ntm, 2.0), __dmul_rn(th, __ddiv_rn(ntm, __dmul_rn(2.0, kPi))));
@@ -123,8 +127,8 @@ __global__ void __launch_bounds__(kThreads) k_compress_variant(const float* __re
         } else {
             // compand_study (analysis.py:404-405)
             const double psi_t = __ddiv_rn(__dadd_rn(th, kPi), __dmul_rn(2.0, kPi));
-            nt = compand_encode(psi_t, V.nt_max, V);
-            nph = compand_encode(__ddiv_rn(ph, kPi), V.np_max, V);
+            nt = compand_encode<KIND>(psi_t, V.nt_max, V);
+            nph = compand_encode<KIND>(__ddiv_rn(ph, kPi), V.np_max, V);
             angles = ((unsigned long long)nph << V.t) | (unsigned long long)nt;
         }
         const unsigned long long field = encode_field(r64, V);
@@ -133,6 +137,14 @@ __global__ void __launch_bounds__(kThreads) k_compress_variant(const float* __re
     if (bad && nonfinite) atomicAdd(nonfinite, bad);
 }
 
+// The reconstruction angles are formed as multiples of pi and their sin/cos
+// taken with sincospi: theta = pi q_t, phi = pi q_p with q_t = 2 psi_t - 1
+// (compander) or 2 n_t / n_t_max - 1 (split), q_p = psi_p or n_p / n_p_max.
+// The reference rounds pi q first and calls sin / cos; the two differ by
+// about one double ulp, so a float32 component differs (by one ulp) only
+// where its double lies within that of a rounding boundary (tests: <= 2 ulp,
+// >= 99.9 % exact).
+template <int KIND>
 __global__ void __launch_bounds__(kThreads) k_decompress_variant(const unsigned long long* __restrict__ w,
                                                                  float* __restrict__ xyz, int64_t n,
                                                                  VParams V) {
@@ -141,24 +153,24 @@ __global__ void __launch_bounds__(kThreads) k_decompress_variant(const unsigned 
         const unsigned long long word = w[i];
         const unsigned long long field = word >> V.shift;
         const unsigned long long angles = word & ((1ull << V.shift) - 1ull);
-        double th2, ph2;
-        if (V.kind == VC3_VARIANT_SPLIT) {
+        double qt, qp;
+        if (KIND == VC3_VARIANT_SPLIT) {
             // joint_decode (analysis.py:294-297) and the reconstruction (:326-333)
             const unsigned long long nt1 = (unsigned long long)(V.nt_max + 1);
             const long long nph = (long long)(angles / nt1), nt = (long long)(angles % nt1);
-            th2 = __dmul_rn(kPi, __dsub_rn(__ddiv_rn(__dmul_rn(2.0, (double)nt), (double)V.nt_max), 1.0));
-            ph2 = __ddiv_rn(__dmul_rn(kPi, (double)nph), (double)V.np_max);
+            qt = __dsub_rn(__ddiv_rn(__dmul_rn(2.0, (double)nt), (double)V.nt_max), 1.0);
+            qp = __ddiv_rn((double)nph, (double)V.np_max);
         } else {
             // compand_study reconstruction (analysis.py:406-414)
             const long long nt = (long long)(angles & ((1ull << V.t) - 1ull));
             const long long nph = (long long)((angles >> V.t) & ((1ull << V.p) - 1ull));
-            th2 = __dsub_rn(__dmul_rn(2.0 * kPi, compand_decode(nt, V.nt_max, V)), kPi);
-            ph2 = __dmul_rn(kPi, compand_decode(nph, V.np_max, V));
+            qt = __dsub_rn(__dmul_rn(2.0, compand_decode<KIND>(nt, V.nt_max, V)), 1.0);
+            qp = compand_decode<KIND>(nph, V.np_max, V);
         }
         const double rh = (double)decode_field(field, V);
         double st, ct, sp, cp;
-        sincos(th2, &st, &ct);
-        sincos(ph2, &sp, &cp);
+        sincospi(qt, &st, &ct);
+        sincospi(qp, &sp, &cp);
         xyz[3 * i] = __double2float_rn(__dmul_rn(__dmul_rn(rh, ct), sp));
         xyz[3 * i + 1] = __double2float_rn(__dmul_rn(__dmul_rn(rh, st), sp));
         xyz[3 * i + 2] = __double2float_rn(__dmul_rn(rh, cp));
@@ -226,8 +238,15 @@ int vc3_compress_variant(const float* xyz, uint64_t* words, int64_t n, vc3_layou
     if (n < 0) return VC3_ERR_ARG;
     if (n == 0) return VC3_OK;
     if (!xyz || !words) return VC3_ERR_ARG;
-    k_compress_variant<<<grid_for_n(n), kThreads, 0, (cudaStream_t)stream>>>(
-        xyz, (unsigned long long*)words, n, V, d_nonfinite);
+    const unsigned g = grid_for_n(n);
+    cudaStream_t s = (cudaStream_t)stream;
+    auto out = (unsigned long long*)words;
+    switch (V.kind) {
+        case VC3_VARIANT_COSINE: k_compress_variant<VC3_VARIANT_COSINE><<<g, kThreads, 0, s>>>(xyz, out, n, V, d_nonfinite); break;
+        case VC3_VARIANT_TANH: k_compress_variant<VC3_VARIANT_TANH><<<g, kThreads, 0, s>>>(xyz, out, n, V, d_nonfinite); break;
+        case VC3_VARIANT_SPLIT: k_compress_variant<VC3_VARIANT_SPLIT><<<g, kThreads, 0, s>>>(xyz, out, n, V, d_nonfinite); break;
+        default: k_compress_variant<VC3_VARIANT_UNIFORM><<<g, kThreads, 0, s>>>(xyz, out, n, V, d_nonfinite);
+    }
     return cudaGetLastError() == cudaSuccess ? VC3_OK : VC3_ERR_CUDA;
 }
 
@@ -239,8 +258,15 @@ int vc3_decompress_variant(const uint64_t* words, float* xyz, int64_t n, vc3_lay
     if (n < 0) return VC3_ERR_ARG;
     if (n == 0) return VC3_OK;
     if (!xyz || !words) return VC3_ERR_ARG;
-    k_decompress_variant<<<grid_for_n(n), kThreads, 0, (cudaStream_t)stream>>>(
-        (const unsigned long long*)words, xyz, n, V);
+    const unsigned g = grid_for_n(n);
+    cudaStream_t s = (cudaStream_t)stream;
+    auto in = (const unsigned long long*)words;
+    switch (V.kind) {
+        case VC3_VARIANT_COSINE: k_decompress_variant<VC3_VARIANT_COSINE><<<g, kThreads, 0, s>>>(in, xyz, n, V); break;
+        case VC3_VARIANT_TANH: k_decompress_variant<VC3_VARIANT_TANH><<<g, kThreads, 0, s>>>(in, xyz, n, V); break;
+        case VC3_VARIANT_SPLIT: k_decompress_variant<VC3_VARIANT_SPLIT><<<g, kThreads, 0, s>>>(in, xyz, n, V); break;
+        default: k_decompress_variant<VC3_VARIANT_UNIFORM><<<g, kThreads, 0, s>>>(in, xyz, n, V);
+    }
     return cudaGetLastError() == cudaSuccess ? VC3_OK : VC3_ERR_CUDA;
 }
 
