@@ -17,7 +17,8 @@ import sys
 
 
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-         "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
+         "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,
+         "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
 
 
 def raw(path: str) -> tuple[list[str], list[str], list[str]]:
