@@ -303,14 +303,16 @@ int launch_add(const unsigned long long* a, const unsigned long long* b, unsigne
         auto fn = exact ? k_add_as<true, DefaultLayout, 2> : k_add_as<false, DefaultLayout, 2>;
         return launch_table_kernel<2>(fn, P, n, vec, s, a, b, c, n, P, vec, tab, full);
     }
-    if (cfg == 1) {
-        auto fn = def ? (exact ? k_add_as<true, DefaultLayout, 1> : k_add_as<false, DefaultLayout, 1>)
-                      : (exact ? k_add_as<true, RuntimeLayout, 1> : k_add_as<false, RuntimeLayout, 1>);
-        return launch_table_kernel<1>(fn, P, n, vec, s, a, b, c, n, P, vec, tab, full);
+#ifdef VC3_TUNE
+    if (cfg == 0) {  // the round's first form, 3 x 256 threads (A/B builds only)
+        auto fn = def ? (exact ? k_add_as<true, DefaultLayout> : k_add_as<false, DefaultLayout>)
+                      : (exact ? k_add_as<true, RuntimeLayout> : k_add_as<false, RuntimeLayout>);
+        return launch_table_kernel<0>(fn, P, n, vec, s, a, b, c, n, P, vec, tab, full);
     }
-    auto fn = def ? (exact ? k_add_as<true, DefaultLayout> : k_add_as<false, DefaultLayout>)
-                  : (exact ? k_add_as<true, RuntimeLayout> : k_add_as<false, RuntimeLayout>);
-    return launch_table_kernel<0>(fn, P, n, vec, s, a, b, c, n, P, vec, tab, full);
+#endif
+    auto fn = def ? (exact ? k_add_as<true, DefaultLayout, 1> : k_add_as<false, DefaultLayout, 1>)
+                  : (exact ? k_add_as<true, RuntimeLayout, 1> : k_add_as<false, RuntimeLayout, 1>);
+    return launch_table_kernel<1>(fn, P, n, vec, s, a, b, c, n, P, vec, tab, full);
 }
 
 int launch_axpy(float al, const unsigned long long* x, const unsigned long long* y,
@@ -321,14 +323,16 @@ int launch_axpy(float al, const unsigned long long* x, const unsigned long long*
         auto fn = exact ? k_axpy_as<true, DefaultLayout, 2> : k_axpy_as<false, DefaultLayout, 2>;
         return launch_table_kernel<2>(fn, P, n, vec, s, al, x, y, yo, n, P, vec, tab, full);
     }
-    if (cfg == 1) {
-        auto fn = def ? (exact ? k_axpy_as<true, DefaultLayout, 1> : k_axpy_as<false, DefaultLayout, 1>)
-                      : (exact ? k_axpy_as<true, RuntimeLayout, 1> : k_axpy_as<false, RuntimeLayout, 1>);
-        return launch_table_kernel<1>(fn, P, n, vec, s, al, x, y, yo, n, P, vec, tab, full);
+#ifdef VC3_TUNE
+    if (cfg == 0) {  // the round's first form, 3 x 256 threads (A/B builds only)
+        auto fn = def ? (exact ? k_axpy_as<true, DefaultLayout> : k_axpy_as<false, DefaultLayout>)
+                      : (exact ? k_axpy_as<true, RuntimeLayout> : k_axpy_as<false, RuntimeLayout>);
+        return launch_table_kernel<0>(fn, P, n, vec, s, al, x, y, yo, n, P, vec, tab, full);
     }
-    auto fn = def ? (exact ? k_axpy_as<true, DefaultLayout> : k_axpy_as<false, DefaultLayout>)
-                  : (exact ? k_axpy_as<true, RuntimeLayout> : k_axpy_as<false, RuntimeLayout>);
-    return launch_table_kernel<0>(fn, P, n, vec, s, al, x, y, yo, n, P, vec, tab, full);
+#endif
+    auto fn = def ? (exact ? k_axpy_as<true, DefaultLayout, 1> : k_axpy_as<false, DefaultLayout, 1>)
+                  : (exact ? k_axpy_as<true, RuntimeLayout, 1> : k_axpy_as<false, RuntimeLayout, 1>);
+    return launch_table_kernel<1>(fn, P, n, vec, s, al, x, y, yo, n, P, vec, tab, full);
 }
 
 int launch_rk(float ca, float cb, float dt, unsigned long long* q, unsigned long long* dq,
@@ -339,14 +343,16 @@ int launch_rk(float ca, float cb, float dt, unsigned long long* q, unsigned long
         auto fn = exact ? k_rk_as<true, DefaultLayout, 2> : k_rk_as<false, DefaultLayout, 2>;
         return launch_table_kernel<2>(fn, P, n, vec, s, ca, cb, dt, q, dq, R, n, P, vec, tab, full);
     }
-    if (cfg == 1) {
-        auto fn = def ? (exact ? k_rk_as<true, DefaultLayout, 1> : k_rk_as<false, DefaultLayout, 1>)
-                      : (exact ? k_rk_as<true, RuntimeLayout, 1> : k_rk_as<false, RuntimeLayout, 1>);
-        return launch_table_kernel<1>(fn, P, n, vec, s, ca, cb, dt, q, dq, R, n, P, vec, tab, full);
+#ifdef VC3_TUNE
+    if (cfg == 0) {  // the round's first form, 3 x 256 threads (A/B builds only)
+        auto fn = def ? (exact ? k_rk_as<true, DefaultLayout> : k_rk_as<false, DefaultLayout>)
+                      : (exact ? k_rk_as<true, RuntimeLayout> : k_rk_as<false, RuntimeLayout>);
+        return launch_table_kernel<0>(fn, P, n, vec, s, ca, cb, dt, q, dq, R, n, P, vec, tab, full);
     }
-    auto fn = def ? (exact ? k_rk_as<true, DefaultLayout> : k_rk_as<false, DefaultLayout>)
-                  : (exact ? k_rk_as<true, RuntimeLayout> : k_rk_as<false, RuntimeLayout>);
-    return launch_table_kernel<0>(fn, P, n, vec, s, ca, cb, dt, q, dq, R, n, P, vec, tab, full);
+#endif
+    auto fn = def ? (exact ? k_rk_as<true, DefaultLayout, 1> : k_rk_as<false, DefaultLayout, 1>)
+                  : (exact ? k_rk_as<true, RuntimeLayout, 1> : k_rk_as<false, RuntimeLayout, 1>);
+    return launch_table_kernel<1>(fn, P, n, vec, s, ca, cb, dt, q, dq, R, n, P, vec, tab, full);
 }
 
 // The all-single compress (layouts with t <= 25, p <= 24: clamp-free buckets).
